@@ -1,0 +1,198 @@
+/*
+ * fdmoe.h — C ABI of the B200-native FlashDMoE operator (libfdmoe.so).
+ *
+ * Drop-in boundary for the reference's operator API
+ *   moefabric::forward(const MoeConfig&, const std::vector<TokenMatrix>& shards,
+ *                      const ModelWeights&, const ForwardOptions&) -> ForwardResult
+ *   (/root/reference/proj/include/moefabric/runtime.hpp:802-1002).
+ * include/moefabric_b200.hpp restates that C++ API on top of these entry points; the
+ * Python host mirror (paper_2506_04667_b200/) binds them with ctypes.
+ *
+ * Plain pointers and sizes only: no torch or CUDA runtime types in the signatures
+ * (streams are passed as void*). Every entry point returns an fdmoe_status; the message
+ * of the last failure on the calling thread is available from fdmoe_last_error().
+ *
+ * Status codes map 1:1 to the reference's exception types (config.hpp:16-30):
+ *   FDMOE_ERR_CONFIG   <-> ConfigError   (shape / configuration errors)
+ *   FDMOE_ERR_PROTOCOL <-> ProtocolError (invalid one-sided write, double signal)
+ *   FDMOE_ERR_RUNTIME  <-> RuntimeFault  (device watchdog expired, accounting mismatch)
+ *   FDMOE_ERR_CUDA     -- CUDA runtime/driver failure (no reference equivalent)
+ *   FDMOE_ERR_UNSUPPORTED -- valid for the reference but outside this operator's envelope
+ *
+ * A handle owns one or more "ranks" (the reference's simulated devices, config.hpp:54-75).
+ * Ranks may live on distinct GPUs of this process, on one GPU ("virtual ranks": CTAs of a
+ * single persistent launch are partitioned by rank; the exchange protocol is unchanged),
+ * or in other processes (one rank per process; peers attached with fdmoe_import_peers).
+ * A handle is not re-entrant: one in-flight forward per handle.
+ */
+#ifndef FDMOE_H
+#define FDMOE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FDMOE_ABI_VERSION 1
+
+typedef enum fdmoe_status {
+    FDMOE_OK = 0,
+    FDMOE_ERR_CONFIG = 1,
+    FDMOE_ERR_PROTOCOL = 2,
+    FDMOE_ERR_RUNTIME = 3,
+    FDMOE_ERR_CUDA = 4,
+    FDMOE_ERR_UNSUPPORTED = 5
+} fdmoe_status;
+
+/* config.hpp:32 Activation */
+typedef enum fdmoe_activation { FDMOE_RELU = 0, FDMOE_GELU = 1, FDMOE_IDENTITY = 2 } fdmoe_activation;
+
+/* Arithmetic of the expert FFN. The gate/routing is FP32-exact in both modes. */
+typedef enum fdmoe_precision {
+    FDMOE_FP32 = 0, /* FP32-accurate: 3xTF32 split on tcgen05 (hi*hi + hi*lo + lo*hi) */
+    FDMOE_BF16 = 1  /* bf16 operands, FP32 accumulation */
+} fdmoe_precision;
+
+typedef enum fdmoe_where { FDMOE_HOST = 0, FDMOE_DEVICE = 1 } fdmoe_where;
+
+/* MoeConfig (config.hpp:53-87), field for field, plus the GPU precision mode. */
+typedef struct fdmoe_config {
+    int64_t tokens_per_device; /* S */
+    int64_t embed_dim;         /* H */
+    int64_t ffn_dim;           /* D */
+    int64_t experts_total;     /* E_total */
+    int64_t devices;           /* P */
+    int64_t topk;              /* k */
+    double capacity_factor;    /* cf */
+    int64_t tile_rows;         /* bM (reference tile; sizes the padded capacity C' only) */
+    int64_t tile_cols;         /* bN (reference tile; accounting only) */
+    int32_t activation;        /* fdmoe_activation */
+    int32_t precision;         /* fdmoe_precision */
+    uint64_t seed;
+} fdmoe_config;
+
+/* ForwardOptions (runtime.hpp:86-92). processors/mode/straggler are accepted for source
+ * compatibility; on the GPU the persistent launch uses every co-resident CTA. */
+typedef struct fdmoe_options {
+    int32_t processors;         /* reference processor threads per device (ignored) */
+    int32_t sequential;         /* ScheduleMode::sequential (bulk-synchronous baseline) */
+    int64_t deadlock_budget_ms; /* in-kernel watchdog budget (runtime.hpp:90, default 5000) */
+} fdmoe_options;
+
+/* Per-rank routing surface (GateOutput, gate.hpp:24-37). All host pointers, nullable.
+ * g_phi: S x E; table_token / table_weight: E x C (token -1 = empty slot);
+ * slot_counts: E; dropped: 2 * S * k int64 (token, expert) pairs in the reference's
+ * emission order (ascending token, pick order); n_dropped: 1.
+ * picks_expert / picks_slot / picks_weight: S x k (slot -1 = capacity-dropped). */
+typedef struct fdmoe_routing {
+    float* g_phi;
+    int64_t* table_token;
+    float* table_weight;
+    int64_t* slot_counts;
+    int64_t* dropped;
+    int64_t* n_dropped;
+    int32_t* picks_expert;
+    int32_t* picks_slot;
+    float* picks_weight;
+} fdmoe_routing;
+
+/* TaskStats (runtime.hpp:94-106) with GPU meaning, per local rank:
+ * gemm0/gemm1 = 128-row FFN tiles executed, combine = combine tasks,
+ * launches = kernel launches this forward (1). bytes / bytes_padded are the P x P
+ * efficient / padded-baseline payload matrices (pgas.hpp:130-147). */
+typedef struct fdmoe_stats {
+    int64_t gemm0, gemm1, combine, enqueued, executed;
+    int64_t bound_initial, bound_final, scheduled_final, launches;
+    double kernel_ms;     /* device time of the layer launch on this rank (CUDA events) */
+} fdmoe_stats;
+
+typedef struct fdmoe_handle fdmoe_handle;
+
+/* ---- pure functions (no GPU needed) --------------------------------------- */
+int32_t fdmoe_abi_version(void);
+const char* fdmoe_last_error(void);
+/* MoeConfig::validate (config.hpp:68-86) plus this operator's envelope checks when
+ * gpu_envelope != 0 (returns FDMOE_ERR_UNSUPPORTED with a message). */
+fdmoe_status fdmoe_config_validate(const fdmoe_config* cfg, int32_t gpu_envelope);
+int64_t fdmoe_expert_capacity(const fdmoe_config* cfg);               /* config.hpp:94 */
+int64_t fdmoe_padded_capacity(int64_t capacity, int64_t tile_rows);   /* config.hpp:104 */
+uint64_t fdmoe_size_L(const fdmoe_config* cfg);                       /* layout.hpp:106 */
+/* layout.hpp:67-79: element offset of slot row (p*, round, buffer, expert, slot) in the
+ * reference layout L (P x 2 x 2 x E_local x C' x H); -1 when out of bounds. */
+int64_t fdmoe_flat_index(int64_t devices, int64_t local_experts, int64_t slot_capacity,
+                         int64_t embed_dim, int64_t p_star, int64_t round, int64_t buffer,
+                         int64_t expert, int64_t slot);
+/* layout.hpp:91-100: 0 ok, 1 = rule 1 violated, 2 = rule 2 violated. */
+int32_t fdmoe_validate_write(int64_t src, int64_t dst, int64_t p_star, int64_t buffer);
+/* runtime.hpp:122-165 task-count arithmetic (reference tile grid bM x bN). */
+int64_t fdmoe_gemm_tasks_for_rows(const fdmoe_config* cfg, int64_t rows);
+int64_t fdmoe_combine_tiles_for_rows(const fdmoe_config* cfg, int64_t rows);
+int64_t fdmoe_initial_task_bound(const fdmoe_config* cfg);
+
+/* Seeded synthetic model / shards, restating harness.hpp:76-109 bit for bit
+ * (std::mt19937_64 + std::normal_distribution<float>). Layouts: wg H x E; w1 E x H x D;
+ * b1 E x D; w2 E x D x H; b2 E x H; shards P x S x H. */
+fdmoe_status fdmoe_synth_model(const fdmoe_config* cfg, uint64_t seed, float* wg, float* w1,
+                               float* b1, float* w2, float* b2);
+fdmoe_status fdmoe_synth_shards(const fdmoe_config* cfg, uint64_t seed, float* shards);
+
+/* ---- operator --------------------------------------------------------------- */
+/* Create the ranks [first_rank, first_rank + n_local) of a cfg->devices-rank group.
+ * device_ids[i] is the CUDA device of local rank i (repeats allowed: virtual ranks).
+ * Allocates each rank's symmetric heap and scratch, one launch group per device. */
+fdmoe_status fdmoe_create(const fdmoe_config* cfg, const int32_t* device_ids, int32_t n_local,
+                          int32_t first_rank, fdmoe_handle** out);
+fdmoe_status fdmoe_destroy(fdmoe_handle* h);
+
+/* Multi-process attach: export this handle's (single) rank heap as an opaque blob of
+ * fdmoe_ipc_size() bytes; import all ranks' blobs (rank-major, world x size). */
+size_t fdmoe_ipc_size(void);
+fdmoe_status fdmoe_export_heap(fdmoe_handle* h, void* blob);
+fdmoe_status fdmoe_import_peers(fdmoe_handle* h, const void* blobs, int32_t world);
+
+/* ModelWeights (config.hpp:130-147) for all E_total experts; each local rank uploads
+ * its own E_local experts (device p owns [p*E_local, (p+1)*E_local), config.hpp:66) and
+ * repacks them K-major (and tf32 hi/lo or bf16) once. Layouts as fdmoe_synth_model. */
+fdmoe_status fdmoe_set_weights(fdmoe_handle* h, const float* wg, const float* w1, const float* b1,
+                               const float* w2, const float* b2, int32_t where);
+
+/* One MoE-layer forward: exactly one persistent kernel launch per device.
+ * in_shards / out_shards: n_local pointers to S x H FP32 (host or device per `where`).
+ * routing / stats: arrays of n_local entries, nullable. Synchronous. */
+fdmoe_status fdmoe_forward(fdmoe_handle* h, const float* const* in_shards, float* const* out_shards,
+                           int32_t where, const fdmoe_options* opts, fdmoe_routing* routing,
+                           fdmoe_stats* stats);
+/* Asynchronous device-pointer variant: enqueue on streams[i] (cudaStream_t as void*,
+ * one per local rank; NULL = the handle's own stream). Pair with fdmoe_sync. */
+fdmoe_status fdmoe_forward_async(fdmoe_handle* h, const float* const* in_dev, float* const* out_dev,
+                                 void* const* streams);
+/* Wait for the last forward, check the device watchdog/error word. */
+fdmoe_status fdmoe_sync(fdmoe_handle* h);
+
+/* Introspection for tests/bench. */
+typedef struct fdmoe_info {
+    int64_t capacity;       /* C */
+    int64_t packet_rows;    /* rows reserved per (source, expert) packet in the receive buffer */
+    int64_t heap_bytes;     /* symmetric heap per rank */
+    int64_t scratch_bytes;  /* private device scratch per rank */
+    int64_t weight_bytes;   /* resident expert weights per rank */
+    int32_t ctas_per_rank;
+    int32_t smem_bytes;
+    int32_t num_sms;
+    int32_t ranks_per_launch;
+} fdmoe_info;
+fdmoe_status fdmoe_get_info(fdmoe_handle* h, fdmoe_info* info);
+
+/* ---- diagnostics (tests only; not part of the reference surface) -------------------- */
+/* The kernel's glibc-expf restatement on n host floats (runs on device 0). */
+fdmoe_status fdmoe_debug_expf(const float* x, float* y, int64_t n);
+/* One 128x256 tile through the layer's TMA -> tcgen05.mma -> TMEM path:
+ * D[128 x 256] = A[128 x K] * B[256 x K]^T, host row-major FP32 (K % 64 == 0). */
+fdmoe_status fdmoe_debug_gemm(int32_t precision, int32_t K, const float* A, const float* B, float* D);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FDMOE_H */

@@ -1,0 +1,256 @@
+// fdmoe_device.cuh — sm_100a PTX wrappers (mbarrier, TMA, tcgen05/TMEM, scoped
+// flags) and the launch-parameter structs shared by the host runtime and kernels.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+namespace fdmoe {
+
+// ---------------------------------------------------------------- constants
+constexpr int kThreads = 256;       // 8 warps: w0 TMA, w1 MMA, w2 TMEM alloc, w4-7 epilogue
+constexpr int kBM = 128;            // rows per FFN tile (TMEM lanes)
+constexpr int kBN = 256;            // columns per FFN tile (TMEM columns per accumulator)
+constexpr int kAccStages = 2;       // TMEM accumulators (2 x 256 = all 512 columns)
+constexpr int kTaskRing = 4;        // producer -> MMA/epilogue task ring
+constexpr int kGateTok = 32;        // tokens per gate block
+constexpr int kGateKC = 32;         // K chunk of the exact gate
+constexpr int kMaxExperts = 256;    // E_total envelope of the exact SIMT gate
+constexpr int kMaxRanks = 64;       // P envelope (peer table size)
+constexpr int kMaxSrcPerTile = 8;   // packet_rows >= 16 -> <= 8 packets per 128-row tile
+constexpr int kCombineTok = 32;     // tokens per combine task
+constexpr int kMaxLocalRanks = 8;   // ranks per launch (virtual ranks on one GPU)
+
+enum Prec : int { kFP32 = 0, kBF16 = 1 };
+
+// Byte offsets inside one rank's symmetric heap (identical on every rank).
+struct HeapLayout {
+    uint64_t x[2][2];     // [parity][hi|lo] receive buffer (bf16: [parity][0] only)
+    uint64_t yc;          // combine-in rows: [E_total][C][H] fp32
+    uint64_t dflag[2];    // [parity] -> [E_local][P] u64 dispatch signals
+    uint64_t cflag[2];    // [parity] -> [E_total][RBF][NB1] u64 combine tile signals
+    uint64_t bytes;
+};
+
+// Everything one rank's kernel needs. Lives in device global memory (64B aligned
+// so the embedded TMA descriptors are valid operands of cp.async.bulk.tensor).
+struct alignas(64) RankCtx {
+    CUtensorMap tm_x[2][2];    // [parity][hi|lo]  rows = E_local*RP, cols = H
+    CUtensorMap tm_c1[2];      // [hi|lo]          rows = E_local*RP, cols = D
+    CUtensorMap tm_w1[2];      // [hi|lo]          rows = E_local*D,  cols = H (W1^T, K-major)
+    CUtensorMap tm_w2[2];      // [hi|lo]          rows = E_local*H,  cols = D (W2^T, K-major)
+
+    uint8_t* peer_heap[kMaxRanks];   // heap base of rank q as mapped here (q == rank: own)
+    HeapLayout hl;
+
+    // private scratch
+    void* c1[2];               // GEMM0 output (hi|lo or bf16)
+    const float* b1;           // [E_local][D]
+    const float* b2;           // [E_local][H]
+    const float* wg;           // [H][E_total]
+    float* g_phi;              // [S][E_total]
+    int32_t* pick_e;           // [S][k]
+    int32_t* pick_slot;        // [S][k]  (-1 = capacity-dropped)
+    float* pick_w;             // [S][k]
+    int32_t* cnt_cta;          // [ctas][E_total] per-CTA expert pick counts
+    int32_t* tbl_tok;          // [E_total][C]
+    float* tbl_w;              // [E_total][C]
+    int32_t* slot_counts;      // [E_total]
+    // control block (rank-local)
+    unsigned long long* bar;   // grid barrier counter (monotonic across launches)
+    uint32_t* gemm_head;
+    uint32_t* comb_head;
+    uint32_t* sent;            // [E_total] rows dispatched so far (last-arriver signals)
+    uint32_t* g0done;          // [E_local][MT] GEMM0 tiles completed per row tile
+    uint32_t* err;             // [4] error word: code, where, a, b
+    unsigned long long* stats; // [8] gemm0, gemm1, combine tasks, dispatch rows, ...
+    int32_t rank;
+};
+
+struct LaunchParams {
+    RankCtx* ranks;            // device array, one per rank in this launch
+    const float* in[kMaxLocalRanks];
+    float* out[kMaxLocalRanks];
+    // shape
+    int S, H, D, E, El, P, k, C, Cp, RP, MT, RBF, NB0, NB1;
+    int act, prec;
+    int ctas_per_rank, nranks;
+    uint32_t epoch;            // 1-based forward counter (same on every rank)
+    unsigned long long launch_seq;   // barrier generation
+    unsigned long long budget_ns;    // watchdog budget
+    uint32_t* abort_flag;      // per launch-group abort word
+    int sequential;            // bulk-synchronous schedule (grid barrier after each phase)
+};
+
+// Error codes written to RankCtx::err[0] (mirrors the reference's exceptions).
+enum DevErr : uint32_t { kErrNone = 0, kErrTimeout = 1, kErrProtocol = 2, kErrAccounting = 3 };
+
+#ifdef __CUDACC__
+// ---------------------------------------------------------------- misc PTX
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const unsigned long long* p) {
+    uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, uint64_t v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_gpu_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint64_t ld_acquire_gpu_u64(const unsigned long long* p) {
+    uint64_t v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ---------------------------------------------------------------- mbarrier
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// Wait with an escape hatch: every 4096 probes check the launch-group abort word and a
+// hard 20 s ceiling (a lost TMA completion must not wedge the GPU).
+__device__ __forceinline__ bool mbar_wait(uint64_t* bar, uint32_t parity, uint32_t* abort_flag) {
+    if (mbar_try_wait(bar, parity)) return true;
+    const uint64_t t0 = globaltimer();
+    uint32_t n = 0;
+    while (!mbar_try_wait(bar, parity)) {
+        if ((++n & 4095u) == 0) {
+            if (ld_volatile_u32(abort_flag) != 0) return false;
+            if (globaltimer() - t0 > 20000000000ull) {
+                atomicExch(abort_flag, 1u);
+                return false;
+            }
+        }
+    }
+    return true;
+}
+
+// ---------------------------------------------------------------- TMA
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap* m) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(m) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* m, uint64_t* bar, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+        ::"r"(smem_u32(dst)), "l"(m), "r"(smem_u32(bar)), "r"(x), "r"(y)
+        : "memory");
+}
+
+// ---------------------------------------------------------------- tcgen05
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+                 "r"(ncols)
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_relinquish() {
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+// 32 lanes x 32 consecutive 32-bit columns: thread t of the warp gets its lane's row.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// UMMA shared-memory matrix descriptor, K-major operand staged by TMA with
+// SWIZZLE_{128,64}B: start>>4 [0,14), LBO>>4 [16,30) (unused for swizzled K-major),
+// SBO>>4 [32,46) = 8 rows x swizzle width, version 1 [46,48), layout [61,64).
+__device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t smem_addr, uint32_t swizzle_bytes) {
+    const uint64_t layout = swizzle_bytes == 128 ? 2ull : (swizzle_bytes == 64 ? 4ull : 6ull);
+    const uint64_t sbo = 8ull * swizzle_bytes;
+    return (uint64_t)((smem_addr >> 4) & 0x3FFF) | (1ull << 16) | (((sbo >> 4) & 0x3FFF) << 32) |
+           (1ull << 46) | (layout << 61);
+}
+// Instruction descriptor: D=f32 [4,6)=1, A/B format [7,10)/[10,13) (1=bf16, 2=tf32),
+// K-major A/B, N>>3 at [17,23), M>>4 at [24,29).
+__host__ __device__ constexpr uint32_t umma_idesc(uint32_t ab_format, uint32_t M, uint32_t N) {
+    return (1u << 4) | (ab_format << 7) | (ab_format << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+#endif  // __CUDACC__
+
+}  // namespace fdmoe

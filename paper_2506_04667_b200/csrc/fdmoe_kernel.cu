@@ -1,0 +1,1072 @@
+// fdmoe_kernel.cu — the FlashDMoE MoE-layer forward as ONE persistent sm_100a kernel
+// per GPU. Phases inside the single launch:
+//
+//   1. exact gate        logits (sequential FP32, as gate.hpp:77-81), softmax with a
+//                        bit-exact restatement of glibc expf (gate.hpp:82-89), top-k on
+//                        probabilities with lower-index tie-break (gate.hpp:41-51, 91),
+//                        combine weights over all k picks (gate.hpp:92-95)
+//      -- rank-local grid barrier (slot assignment needs every token's picks) --
+//   2. slots + dispatch  capacity slots in ascending token order (gate.hpp:94-103) via
+//                        per-CTA prefix counts; each kept row is pushed with 16-byte
+//                        stores straight into the owning rank's receive buffer (peer
+//                        memory over NVLink, or local), tf32 hi/lo-split or bf16; the
+//                        last CTA to finish a packet publishes a release.sys signal
+//                        carrying the row count (zero-row packets signal too,
+//                        runtime.hpp:328-331)
+//   3. expert FFN        tile queue (one atomic head per rank): warp 0 waits for the
+//                        packet signals / GEMM0 row-tile counters, then TMA-streams
+//                        operands into a smem ring; warp 1 issues tcgen05.mma into
+//                        double-buffered TMEM accumulators; warps 4-7 drain TMEM:
+//                        GEMM0 epilogue = +b1, activation, split -> C1 scratch;
+//                        GEMM1 epilogue = +b2, rows stored directly into the ORIGIN
+//                        rank's combine buffer + per-tile release.sys signal
+//                        (runtime.hpp:652-699, pgas.hpp:99-113)
+//   4. combine           per token, O = sum over kept picks in pick order of w * y
+//                        (oracle.hpp:102-107, tiled_blas.hpp:125-135)
+#include <cuda_bf16.h>
+#include <cstdint>
+
+#include "fdmoe_device.cuh"
+
+namespace fdmoe {
+
+// ---------------------------------------------------------------- glibc expf
+// Table-driven expf of glibc (EXP2F_TABLE_BITS = 5), FMA build — restated in
+// oracle/moe_oracle.c:orc_expf_restated and pinned against libm on every float in
+// [-110, 0]. Explicit __fma_rn/__dmul_rn/__dadd_rn so nvcc cannot re-associate.
+__device__ __constant__ unsigned long long c_exp_tab[32] = {
+    0x3ff0000000000000ull, 0x3fefd9b0d3158574ull, 0x3fefb5586cf9890full, 0x3fef9301d0125b51ull,
+    0x3fef72b83c7d517bull, 0x3fef54873168b9aaull, 0x3fef387a6e756238ull, 0x3fef1e9df51fdee1ull,
+    0x3fef06fe0a31b715ull, 0x3feef1a7373aa9cbull, 0x3feedea64c123422ull, 0x3feece086061892dull,
+    0x3feebfdad5362a27ull, 0x3feeb42b569d4f82ull, 0x3feeab07dd485429ull, 0x3feea47eb03a5585ull,
+    0x3feea09e667f3bcdull, 0x3fee9f75e8ec5f74ull, 0x3feea11473eb0187ull, 0x3feea589994cce13ull,
+    0x3feeace5422aa0dbull, 0x3feeb737b0cdc5e5ull, 0x3feec49182a3f090ull, 0x3feed503b23e255dull,
+    0x3feee89f995ad3adull, 0x3feeff76f2fb5e47ull, 0x3fef199bdd85529cull, 0x3fef3720dcef9069ull,
+    0x3fef5818dcfba487ull, 0x3fef7c97337b9b5full, 0x3fefa4afa2a490daull, 0x3fefd0765b6e4540ull,
+};
+
+__device__ __forceinline__ float expf_glibc(float x) {
+    const double inv_ln2_n = 0x1.71547652b82fep+0 * 32.0;
+    const double shift = 0x1.8p+52;
+    const double c0 = 0x1.c6af84b912394p-5 / 32.0 / 32.0 / 32.0;
+    const double c1 = 0x1.ebfce50fac4f3p-3 / 32.0 / 32.0;
+    const double c2 = 0x1.62e42ff0c52d6p-1 / 32.0;
+    const uint32_t ux = __float_as_uint(x);
+    const uint32_t abstop = (ux >> 20) & 0x7ff;
+    if (abstop >= (0x42b00000u >> 20)) {                    // |x| >= 88 or NaN
+        if (ux == 0xff800000u) return 0.0f;                 // -inf
+        if (abstop >= (0x7f800000u >> 20)) return x + x;    // inf / nan
+        if (x > 0x1.62e42ep6f) return __int_as_float(0x7f800000);
+        if (x < -0x1.9fe368p6f) return 0.0f;
+    }
+    const double xd = (double)x;
+    double kd = __fma_rn(inv_ln2_n, xd, shift);
+    const unsigned long long ki = (unsigned long long)__double_as_longlong(kd);
+    kd = __dsub_rn(kd, shift);
+    const double r = __fma_rn(inv_ln2_n, xd, -kd);
+    unsigned long long t = c_exp_tab[ki & 31ull];
+    t += ki << 47;
+    const double s = __longlong_as_double((long long)t);
+    const double z = __fma_rn(c0, r, c1);
+    const double r2 = __dmul_rn(r, r);
+    double y = __fma_rn(c2, r, 1.0);
+    y = __fma_rn(z, r2, y);
+    y = __dmul_rn(y, s);
+    return __double2float_rn(y);
+}
+
+// tiled_blas.hpp:58-67 (erf form of GELU)
+__device__ __forceinline__ float activation(int act, float x) {
+    if (act == 0) return x > 0.0f ? x : 0.0f;
+    if (act == 1) return 0.5f * x * (1.0f + erff(x * 0.70710678118654752440f));
+    return x;
+}
+
+__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
+// ---------------------------------------------------------------- error / watchdog
+__device__ __noinline__ void raise_error(const LaunchParams& P, const RankCtx& R, uint32_t code, uint32_t where,
+                                         uint32_t a, uint32_t b) {
+    if (atomicCAS(R.err, 0u, code) == 0u) {
+        R.err[1] = where;
+        R.err[2] = a;
+        R.err[3] = b;
+    }
+    atomicExch(P.abort_flag, 1u);
+    __threadfence_system();
+}
+
+// Spin until *flag carries this epoch; returns the low 32 bits (count) or -1 on abort/timeout.
+__device__ __forceinline__ int64_t wait_epoch_flag(const LaunchParams& P, const RankCtx& R,
+                                                   const unsigned long long* flag, uint32_t where) {
+    uint64_t v = ld_acquire_sys(flag);
+    if ((uint32_t)(v >> 32) == P.epoch) return (int64_t)(uint32_t)v;
+    const uint64_t t0 = globaltimer();
+    uint32_t n = 0;
+    while (true) {
+        v = ld_acquire_sys(flag);
+        if ((uint32_t)(v >> 32) == P.epoch) return (int64_t)(uint32_t)v;
+        if ((++n & 255u) == 0) {
+            if (ld_volatile_u32(P.abort_flag)) return -1;
+            if (globaltimer() - t0 > P.budget_ns) {
+                raise_error(P, R, kErrTimeout, where, (uint32_t)(v >> 32), (uint32_t)v);
+                return -1;
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ bool wait_counter(const LaunchParams& P, const RankCtx& R, const uint32_t* ctr,
+                                             uint32_t target, uint32_t where) {
+    if (ld_acquire_gpu_u32(ctr) >= target) return true;
+    const uint64_t t0 = globaltimer();
+    uint32_t n = 0;
+    while (ld_acquire_gpu_u32(ctr) < target) {
+        if ((++n & 255u) == 0) {
+            if (ld_volatile_u32(P.abort_flag)) return false;
+            if (globaltimer() - t0 > P.budget_ns) {
+                raise_error(P, R, kErrTimeout, where, target, ld_volatile_u32(ctr));
+                return false;
+            }
+        }
+    }
+    return true;
+}
+
+// Rank-local grid barrier over the co-resident CTAs of one rank (cooperative launch).
+// The counter is monotonic across launches; `gen` is this barrier's global index.
+__device__ bool rank_barrier(const LaunchParams& P, const RankCtx& R, unsigned long long gen) {
+    __shared__ int s_ok;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        s_ok = 1;
+        __threadfence();
+        atomicAdd(R.bar, 1ull);
+        const unsigned long long target = (gen + 1ull) * (unsigned long long)P.ctas_per_rank;
+        const uint64_t t0 = globaltimer();
+        uint32_t n = 0;
+        while (ld_acquire_gpu_u64(R.bar) < target) {
+            if ((++n & 255u) == 0) {
+                if (ld_volatile_u32(P.abort_flag)) { s_ok = 0; break; }
+                if (globaltimer() - t0 > P.budget_ns) {
+                    raise_error(P, R, kErrTimeout, 100, (uint32_t)target, 0);
+                    s_ok = 0;
+                    break;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    return s_ok != 0;
+}
+
+// ================================================================ phase 1: exact gate
+// Smem: sL[kGateTok][Ep] logits/probs, sA[kGateKC][kGateTok] (A chunk, transposed),
+//       sW[kGateKC][Ep] (Wg chunk), sCnt[Ep] CTA-level pick counts.
+__device__ void gate_phase(const LaunchParams& P, const RankCtx& R, const float* __restrict__ A, int cta,
+                           uint8_t* smem) {
+    const int E = P.E, H = P.H, S = P.S, K = P.k;
+    const int Ep = (E + 7) & ~7;
+    float* sL = reinterpret_cast<float*>(smem);
+    float* sA = sL + kGateTok * Ep;
+    float* sW = sA + kGateKC * kGateTok;
+    int* sCnt = reinterpret_cast<int*>(sW + kGateKC * Ep);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int e = tid; e < Ep; e += kThreads) sCnt[e] = 0;
+
+    const int nblk = (S + kGateTok - 1) / kGateTok;
+    const int b0 = (int)((long long)nblk * cta / P.ctas_per_rank);
+    const int b1 = (int)((long long)nblk * (cta + 1) / P.ctas_per_rank);
+    const int n_eg = Ep / 8;                 // expert groups of 8
+    const int n_items = (kGateTok / 2) * n_eg;  // token pairs x expert groups (<= 512)
+
+    for (int blk = b0; blk < b1; ++blk) {
+        const int tok0 = blk * kGateTok;
+        float acc[2][2][8];
+#pragma unroll
+        for (int it = 0; it < 2; ++it)
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[it][i][j] = 0.0f;
+
+        for (int k0 = 0; k0 < H; k0 += kGateKC) {
+            const int kc = min(kGateKC, H - k0);
+            __syncthreads();
+            for (int i = tid; i < kGateTok * kGateKC; i += kThreads) {
+                const int t = i / kGateKC, kk = i % kGateKC;
+                const int tok = tok0 + t;
+                sA[kk * kGateTok + t] = (tok < S && kk < kc) ? A[(size_t)tok * H + k0 + kk] : 0.0f;
+            }
+            for (int i = tid; i < kGateKC * Ep; i += kThreads) {
+                const int kk = i / Ep, e = i % Ep;
+                sW[kk * Ep + e] = (kk < kc && e < E) ? R.wg[(size_t)(k0 + kk) * E + e] : 0.0f;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int it = 0; it < 2; ++it) {
+                const int item = tid + it * kThreads;
+                if (item < n_items) {
+                    const int tg = item / n_eg, eg = item % n_eg;
+                    for (int kk = 0; kk < kc; ++kk) {
+                        const float2 a = *reinterpret_cast<const float2*>(&sA[kk * kGateTok + 2 * tg]);
+                        const float4 w0 = *reinterpret_cast<const float4*>(&sW[kk * Ep + 8 * eg]);
+                        const float4 w1 = *reinterpret_cast<const float4*>(&sW[kk * Ep + 8 * eg + 4]);
+                        const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            acc[it][0][j] = __fadd_rn(acc[it][0][j], __fmul_rn(a.x, wv[j]));
+                            acc[it][1][j] = __fadd_rn(acc[it][1][j], __fmul_rn(a.y, wv[j]));
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int it = 0; it < 2; ++it) {
+            const int item = tid + it * kThreads;
+            if (item < n_items) {
+                const int tg = item / n_eg, eg = item % n_eg;
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) sL[(2 * tg + i) * Ep + 8 * eg + j] = acc[it][i][j];
+            }
+        }
+        __syncthreads();
+
+        // softmax + top-k: one warp per token (4 tokens per warp)
+        for (int t = warp; t < kGateTok; t += kThreads / 32) {
+            const int tok = tok0 + t;
+            if (tok >= S) continue;
+            float* row = sL + t * Ep;
+            // max (exact and order-free; std::max semantics are irrelevant to the
+            // result because only x - max feeds expf and ties give identical values)
+            float mx = row[0];
+            for (int e = lane; e < E; e += 32) mx = fmaxf(mx, row[e]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            for (int e = lane; e < E; e += 32) row[e] = expf_glibc(__fsub_rn(row[e], mx));
+            __syncwarp();
+            float sum = 0.0f;
+            if (lane == 0)
+                for (int e = 0; e < E; ++e) sum = __fadd_rn(sum, row[e]);   // ascending e (gate.hpp:85-88)
+            sum = __shfl_sync(0xffffffffu, sum, 0);
+            for (int e = lane; e < E; e += 32) {
+                const float p = __fdiv_rn(row[e], sum);
+                row[e] = p;
+                R.g_phi[(size_t)tok * E + e] = p;
+            }
+            __syncwarp();
+            // top-k by repeated argmax; ties -> lower expert index
+            uint32_t taken = 0;   // bit j: expert lane + 32*j taken
+            float denom = 0.0f;
+            int pe[8];
+            float pv[8];
+            for (int j = 0; j < K; ++j) {
+                float bv = -1.0f;
+                int bi = 0x7fffffff;
+                for (int e = lane, jj = 0; e < E; e += 32, ++jj) {
+                    if (taken & (1u << jj)) continue;
+                    const float v = row[e];
+                    if (v > bv || (v == bv && e < bi)) { bv = v; bi = e; }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                    if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+                }
+                if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
+                if (j < 8) { pe[j] = bi; pv[j] = bv; }
+                denom = __fadd_rn(denom, bv);   // pick order (gate.hpp:92)
+                if (lane == 0) {
+                    R.pick_e[(size_t)tok * K + j] = bi;
+                    atomicAdd(&sCnt[bi], 1);
+                }
+            }
+            if (lane == 0) {
+                for (int j = 0; j < K; ++j) {
+                    const float p = j < 8 ? pv[j] : row[R.pick_e[(size_t)tok * K + j]];
+                    R.pick_w[(size_t)tok * K + j] = denom > 0.0f ? __fdiv_rn(p, denom) : 0.0f;
+                }
+            }
+            (void)pe;
+        }
+        __syncthreads();
+    }
+    __syncthreads();
+    for (int e = tid; e < E; e += kThreads) R.cnt_cta[(size_t)cta * E + e] = sCnt[e];
+}
+
+// ================================================================ phase 2: slots + dispatch
+__device__ void dispatch_phase(const LaunchParams& P, const RankCtx& R, const float* __restrict__ A, int cta,
+                               uint8_t* smem) {
+    const int E = P.E, H = P.H, S = P.S, K = P.k, C = P.C;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int* sRun = reinterpret_cast<int*>(smem);     // running slot counter per expert
+    int* sN = sRun + kMaxExperts;                  // n_e = min(total, C)
+    int* sKept = sN + kMaxExperts;                 // rows of e kept from this CTA
+    const uint32_t par = P.epoch & 1u;
+    const uint64_t sig_hi = (uint64_t)P.epoch << 32;
+
+    for (int e = tid; e < E; e += kThreads) {
+        int base = 0, tot = 0;
+        for (int c = 0; c < P.ctas_per_rank; ++c) {
+            const int v = R.cnt_cta[(size_t)c * E + e];
+            if (c < cta) base += v;
+            tot += v;
+        }
+        const int mine = R.cnt_cta[(size_t)cta * E + e];
+        const int n = min(tot, C);
+        sRun[e] = base;
+        sN[e] = n;
+        sKept[e] = max(0, min(C - base, mine));
+        if (cta == 0) {
+            R.slot_counts[e] = n;
+            for (int s = n; s < C; ++s) {
+                R.tbl_tok[(size_t)e * C + s] = -1;
+                R.tbl_w[(size_t)e * C + s] = 0.0f;
+            }
+            if (n == 0) {   // zero-row packets still signal (runtime.hpp:328-331)
+                const int q = e / P.El, le = e % P.El;
+                unsigned long long* f = reinterpret_cast<unsigned long long*>(R.peer_heap[q] + R.hl.dflag[par]) +
+                                        (size_t)le * P.P + R.rank;
+                st_release_sys(f, sig_hi);
+            }
+        }
+    }
+    __syncthreads();
+
+    const int nblk = (S + kGateTok - 1) / kGateTok;
+    const int b0 = (int)((long long)nblk * cta / P.ctas_per_rank);
+    const int b1 = (int)((long long)nblk * (cta + 1) / P.ctas_per_rank);
+    const int tokA = b0 * kGateTok, tokB = min(S, b1 * kGateTok);
+
+    // slot assignment in ascending token order (one warp, lane = token in block):
+    // slot = (picks of e by earlier CTAs) + (by earlier blocks of this CTA) + (by earlier
+    // tokens of this block) -- exactly the sequential counter of gate.hpp:94-103.
+    if (warp == 0) {
+        for (int blk = b0; blk < b1; ++blk) {
+            const int tok = blk * kGateTok + lane;
+            const bool valid = tok < S;
+            int mye[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) mye[j] = (valid && j < K) ? R.pick_e[(size_t)tok * K + j] : -1;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (j >= K) break;
+                const int e = mye[j];
+                int rank = 0;
+                for (int t2 = 0; t2 < 32; ++t2) {
+#pragma unroll
+                    for (int j2 = 0; j2 < 8; ++j2) {
+                        if (j2 >= K) break;
+                        const int e2 = __shfl_sync(0xffffffffu, mye[j2], t2);
+                        if (t2 < lane && e2 == e) ++rank;
+                    }
+                }
+                if (valid) {
+                    const int slot = sRun[e] + rank;
+                    if (slot < C) {
+                        R.pick_slot[(size_t)tok * K + j] = slot;
+                        R.tbl_tok[(size_t)e * C + slot] = tok;
+                        R.tbl_w[(size_t)e * C + slot] = R.pick_w[(size_t)tok * K + j];
+                    } else {
+                        R.pick_slot[(size_t)tok * K + j] = -1;
+                    }
+                }
+            }
+            __syncwarp();
+            if (valid)
+                for (int j = 0; j < K; ++j) atomicAdd(&sRun[mye[j]], 1);
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+
+    // push kept rows to the owner's receive buffer (one warp per (token, pick))
+    const int nunits = (tokB - tokA) * K;
+    const int H4 = H >> 2;
+    for (int u = warp; u < nunits; u += kThreads / 32) {
+        const int tok = tokA + u / K, j = u % K;
+        const int slot = R.pick_slot[(size_t)tok * K + j];
+        if (slot < 0) continue;
+        const int e = R.pick_e[(size_t)tok * K + j];
+        const int q = e / P.El, le = e % P.El;
+        const size_t row = (size_t)le * P.RP + (size_t)R.rank * P.Cp + slot;
+        const float4* src = reinterpret_cast<const float4*>(A + (size_t)tok * H);
+        uint8_t* hb = R.peer_heap[q];
+        if (P.prec == kFP32) {
+            float4* dhi = reinterpret_cast<float4*>(hb + R.hl.x[par][0]) + row * H4;
+            float4* dlo = reinterpret_cast<float4*>(hb + R.hl.x[par][1]) + row * H4;
+            for (int c = lane; c < H4; c += 32) {
+                const float4 v = __ldg(src + c);
+                float4 h, l;
+                h.x = tf32_hi(v.x); h.y = tf32_hi(v.y); h.z = tf32_hi(v.z); h.w = tf32_hi(v.w);
+                l.x = __fsub_rn(v.x, h.x); l.y = __fsub_rn(v.y, h.y);
+                l.z = __fsub_rn(v.z, h.z); l.w = __fsub_rn(v.w, h.w);
+                dhi[c] = h;
+                dlo[c] = l;
+            }
+        } else {
+            uint2* d = reinterpret_cast<uint2*>(hb + R.hl.x[par][0]) + row * H4;
+            for (int c = lane; c < H4; c += 32) {
+                const float4 v = __ldg(src + c);
+                __nv_bfloat162 p0 = __floats2bfloat162_rn(v.x, v.y);
+                __nv_bfloat162 p1 = __floats2bfloat162_rn(v.z, v.w);
+                uint2 o;
+                o.x = *reinterpret_cast<uint32_t*>(&p0);
+                o.y = *reinterpret_cast<uint32_t*>(&p1);
+                d[c] = o;
+            }
+        }
+    }
+    __syncthreads();
+    // last CTA to complete a packet publishes its signal (pgas.hpp:99-113 semantics)
+    for (int e = tid; e < E; e += kThreads) {
+        const int kept = sKept[e];
+        if (kept <= 0) continue;
+        __threadfence_system();
+        const uint32_t old = atomicAdd(&R.sent[e], (uint32_t)kept);
+        if ((int)(old + kept) == sN[e]) {
+            __threadfence_system();
+            const int q = e / P.El, le = e % P.El;
+            unsigned long long* f =
+                reinterpret_cast<unsigned long long*>(R.peer_heap[q] + R.hl.dflag[par]) + (size_t)le * P.P + R.rank;
+            st_release_sys(f, sig_hi | (uint32_t)sN[e]);
+        } else if ((int)(old + kept) > sN[e]) {
+            raise_error(P, R, kErrProtocol, 200, e, old + kept);
+        }
+    }
+}
+
+// ================================================================ phase 3: expert FFN
+struct Task {
+    int type;   // 0 = GEMM0, 1 = GEMM1, -1 = end
+    int le, nb, m;
+    int nsrc, src0;
+    int cnt[kMaxSrcPerTile];   // valid rows per packet in the tile
+    int rows_lo[kMaxSrcPerTile];   // first tile row of each packet
+};
+
+template <int PREC>
+struct GemmCfg {
+    static constexpr int BK = PREC == kFP32 ? 32 : 64;          // 128-byte K rows (SWIZZLE_128B)
+    static constexpr int ESZ = PREC == kFP32 ? 4 : 2;
+    static constexpr int A_BYTES = kBM * BK * ESZ;             // one A operand plane
+    static constexpr int B_BYTES = kBN * BK * ESZ;             // one B operand plane
+    static constexpr int PLANES = PREC == kFP32 ? 2 : 1;       // hi/lo split
+    static constexpr int STAGE_BYTES = (A_BYTES + B_BYTES) * PLANES;
+    static constexpr int STAGES = PREC == kFP32 ? 2 : 4;
+    static constexpr int KSTEP = PREC == kFP32 ? 8 : 16;       // K per tcgen05.mma
+    static constexpr uint32_t IDESC = umma_idesc(PREC == kFP32 ? 2u : 1u, kBM, kBN);
+    static constexpr int RING_BYTES = STAGE_BYTES * STAGES;
+    static constexpr int CTRL_BYTES = 1024;
+    static constexpr int SMEM_BYTES = RING_BYTES + CTRL_BYTES;
+};
+
+struct GemmCtrl {
+    uint64_t full[4], empty[4];
+    uint64_t tfull[kAccStages], tempty[kAccStages];
+    uint64_t qfull[kTaskRing], qempty[kTaskRing];
+    uint32_t tmem_base;
+    uint32_t pad;
+    Task ring[kTaskRing];
+};
+
+__device__ __forceinline__ void decode_task(const LaunchParams& P, uint32_t t, uint32_t n_g0, Task& tk) {
+    if (t < n_g0) {
+        tk.type = 0;
+        const uint32_t per_e = (uint32_t)P.NB0 * P.MT;
+        tk.le = t / per_e;
+        const uint32_t r = t % per_e;
+        tk.nb = r / P.MT;
+        tk.m = r % P.MT;
+    } else {
+        t -= n_g0;
+        tk.type = 1;
+        const uint32_t per_e = (uint32_t)P.NB1 * P.MT;
+        tk.le = t / per_e;
+        const uint32_t r = t % per_e;
+        tk.nb = r / P.MT;
+        tk.m = r % P.MT;
+    }
+}
+
+// Packets intersecting row tile m of an expert's receive region, and their signalled rows.
+// Returns total valid rows, or -1 on abort.
+__device__ int resolve_tile_rows(const LaunchParams& P, const RankCtx& R, Task& tk) {
+    const uint32_t par = P.epoch & 1u;
+    const unsigned long long* dflag =
+        reinterpret_cast<const unsigned long long*>(R.peer_heap[R.rank] + R.hl.dflag[par]) + (size_t)tk.le * P.P;
+    int total = 0;
+    if (P.Cp >= kBM) {
+        const int per = P.Cp / kBM;
+        const int src = tk.m / per, rb = tk.m % per;
+        tk.nsrc = 1;
+        tk.src0 = src;
+        const int64_t n = wait_epoch_flag(P, R, dflag + src, 300);
+        if (n < 0) return -1;
+        const int v = max(0, min(kBM, (int)n - rb * kBM));
+        tk.cnt[0] = v;
+        tk.rows_lo[0] = 0;
+        total = v;
+    } else {
+        const int per = kBM / P.Cp;
+        const int s0 = tk.m * per;
+        const int s1 = min(P.P, s0 + per);
+        tk.nsrc = s1 - s0;
+        tk.src0 = s0;
+        for (int s = s0; s < s1; ++s) {
+            const int64_t n = wait_epoch_flag(P, R, dflag + s, 301);
+            if (n < 0) return -1;
+            tk.cnt[s - s0] = (int)n;
+            tk.rows_lo[s - s0] = (s - s0) * P.Cp;
+            total += (int)n;
+        }
+    }
+    return total;
+}
+
+template <int PREC>
+__device__ void gemm_producer(const LaunchParams& P, const RankCtx& R, uint8_t* ring, GemmCtrl& G) {
+    using Cfg = GemmCfg<PREC>;
+    const uint32_t n_g0 = (uint32_t)P.El * P.NB0 * P.MT;
+    const uint32_t n_g1 = (uint32_t)P.El * P.NB1 * P.MT;
+    const uint32_t par = P.epoch & 1u;
+    int stage = 0;
+    uint32_t phase = 0;
+    int q = 0;
+    uint32_t qphase = 0;
+    for (int i = 0; i < 2; ++i) {
+        tma_prefetch(&R.tm_x[par][i]);
+        tma_prefetch(&R.tm_c1[i]);
+        tma_prefetch(&R.tm_w1[i]);
+        tma_prefetch(&R.tm_w2[i]);
+    }
+    while (true) {
+        const uint32_t t = atomicAdd(R.gemm_head, 1u);
+        Task tk;
+        bool end = t >= n_g0 + n_g1;
+        if (!end) {
+            decode_task(P, t, n_g0, tk);
+            const int rows = resolve_tile_rows(P, R, tk);
+            if (rows < 0) end = true;
+            else if (rows == 0) continue;   // empty tile: no GEMM0/GEMM1 work exists for it
+            else if (tk.type == 1) {
+                if (!wait_counter(P, R, R.g0done + (size_t)tk.le * P.MT + tk.m, (uint32_t)P.NB0, 302)) end = true;
+            }
+        }
+        if (!mbar_wait(&G.qempty[q], qphase ^ 1u, P.abort_flag)) end = true;
+        if (end) {
+            G.ring[q].type = -1;
+            mbar_arrive(&G.qfull[q]);
+            break;
+        }
+        G.ring[q] = tk;
+        mbar_arrive(&G.qfull[q]);
+        if (++q == kTaskRing) { q = 0; qphase ^= 1u; }
+
+        // operands: generic-proxy writes (peer dispatch stores / local GEMM0 epilogue)
+        // were acquired above; order them before the async-proxy (TMA) reads.
+        fence_proxy_async_global();
+        const CUtensorMap* ta[2];
+        const CUtensorMap* tb[2];
+        int ya, yb, nk;
+        if (tk.type == 0) {
+            ta[0] = &R.tm_x[par][0]; ta[1] = &R.tm_x[par][1];
+            tb[0] = &R.tm_w1[0]; tb[1] = &R.tm_w1[1];
+            ya = tk.le * P.RP + tk.m * kBM;
+            yb = tk.le * P.D + tk.nb * kBN;
+            nk = (P.H + Cfg::BK - 1) / Cfg::BK;
+        } else {
+            ta[0] = &R.tm_c1[0]; ta[1] = &R.tm_c1[1];
+            tb[0] = &R.tm_w2[0]; tb[1] = &R.tm_w2[1];
+            ya = tk.le * P.RP + tk.m * kBM;
+            yb = tk.le * P.H + tk.nb * kBN;
+            nk = (P.D + Cfg::BK - 1) / Cfg::BK;
+        }
+        for (int kb = 0; kb < nk; ++kb) {
+            if (!mbar_wait(&G.empty[stage], phase ^ 1u, P.abort_flag)) return;
+            uint8_t* st = ring + stage * Cfg::STAGE_BYTES;
+            mbar_expect_tx(&G.full[stage], Cfg::STAGE_BYTES);
+            const int x = kb * Cfg::BK;
+#pragma unroll
+            for (int pl = 0; pl < Cfg::PLANES; ++pl) {
+                tma_load_2d(st + pl * Cfg::A_BYTES, ta[pl], &G.full[stage], x, ya);
+                tma_load_2d(st + Cfg::PLANES * Cfg::A_BYTES + pl * Cfg::B_BYTES, tb[pl], &G.full[stage], x, yb);
+            }
+            if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
+        }
+    }
+}
+
+template <int PREC>
+__device__ void gemm_mma(const LaunchParams& P, uint8_t* ring, GemmCtrl& G) {
+    using Cfg = GemmCfg<PREC>;
+    int stage = 0;
+    uint32_t phase = 0;
+    int q = 0;
+    uint32_t qphase = 0;
+    int acc = 0;
+    uint32_t aphase = 0;
+    const uint32_t tmem = G.tmem_base;
+    while (true) {
+        if (!mbar_wait(&G.qfull[q], qphase, P.abort_flag)) return;
+        const Task& tk = G.ring[q];
+        if (tk.type < 0) return;
+        const int nk = ((tk.type == 0 ? P.H : P.D) + Cfg::BK - 1) / Cfg::BK;
+        if (!mbar_wait(&G.tempty[acc], aphase ^ 1u, P.abort_flag)) return;
+        tc_fence_after();
+        const uint32_t d_tmem = tmem + (uint32_t)(acc * kBN);
+        for (int kb = 0; kb < nk; ++kb) {
+            if (!mbar_wait(&G.full[stage], phase, P.abort_flag)) return;
+            tc_fence_after();
+            const uint32_t base = smem_u32(ring + stage * Cfg::STAGE_BYTES);
+#pragma unroll
+            for (int ks = 0; ks < Cfg::BK / Cfg::KSTEP; ++ks) {
+                const uint32_t koff = ks * Cfg::KSTEP * Cfg::ESZ;   // 32 bytes inside the 128B swizzle atom
+                const uint64_t a0 = umma_desc_kmajor(base + koff, 128);
+                const uint64_t b0 = umma_desc_kmajor(base + Cfg::PLANES * Cfg::A_BYTES + koff, 128);
+                const uint32_t accum = (kb | ks) != 0 ? 1u : 0u;
+                if (PREC == kFP32) {
+                    const uint64_t a1 = umma_desc_kmajor(base + Cfg::A_BYTES + koff, 128);
+                    const uint64_t b1 = umma_desc_kmajor(base + Cfg::PLANES * Cfg::A_BYTES + Cfg::B_BYTES + koff, 128);
+                    // 3xTF32: lo*hi + hi*lo + hi*hi (small terms first)
+                    mma_tf32(d_tmem, a1, b0, Cfg::IDESC, accum);
+                    mma_tf32(d_tmem, a0, b1, Cfg::IDESC, 1u);
+                    mma_tf32(d_tmem, a0, b0, Cfg::IDESC, 1u);
+                } else {
+                    mma_bf16(d_tmem, a0, b0, Cfg::IDESC, accum);
+                }
+            }
+            mma_commit(&G.empty[stage]);   // smem slot free once these MMAs retire
+            if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
+        }
+        mma_commit(&G.tfull[acc]);         // accumulator ready for the epilogue
+        mbar_arrive(&G.qempty[q]);
+        if (++q == kTaskRing) { q = 0; qphase ^= 1u; }
+        if (++acc == kAccStages) { acc = 0; aphase ^= 1u; }
+    }
+}
+
+template <int PREC>
+__device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl& G, unsigned long long* stat) {
+    const int et = threadIdx.x - 128;   // 0..127 == TMEM lane == tile row
+    const int wq = et >> 5;
+    const uint32_t par = P.epoch & 1u;
+    int q = 0;
+    uint32_t qphase = 0;
+    int acc = 0;
+    uint32_t aphase = 0;
+    const uint32_t tmem = G.tmem_base;
+    const int e_glob_base = R.rank * P.El;
+    while (true) {
+        if (!mbar_wait(&G.qfull[q], qphase, P.abort_flag)) return;
+        const Task tk = G.ring[q];
+        if (tk.type < 0) return;
+        if (!mbar_wait(&G.tfull[acc], aphase, P.abort_flag)) return;
+        tc_fence_after();
+
+        // which packet does my row belong to, and is it a valid (signalled) row?
+        int src = -1, slot = 0;
+        bool valid = false;
+        if (P.Cp >= kBM) {
+            src = tk.src0;
+            slot = (tk.m % (P.Cp / kBM)) * kBM + et;
+            valid = et < tk.cnt[0];
+        } else {
+            const int j = et / P.Cp;
+            if (j < tk.nsrc) {
+                src = tk.src0 + j;
+                slot = et - j * P.Cp;
+                valid = slot < tk.cnt[j];
+            }
+        }
+        const size_t grow = (size_t)tk.le * P.RP + (size_t)tk.m * kBM + et;   // row in X / C1
+        const int ncols = tk.type == 0 ? P.D : P.H;
+        const float* bias = (tk.type == 0 ? R.b1 + (size_t)tk.le * P.D : R.b2 + (size_t)tk.le * P.H) + tk.nb * kBN;
+        const int e_glob = e_glob_base + tk.le;
+        float* ydst = nullptr;
+        if (tk.type == 1 && valid)
+            ydst = reinterpret_cast<float*>(R.peer_heap[src] + R.hl.yc) + ((size_t)e_glob * P.C + slot) * P.H +
+                   (size_t)tk.nb * kBN;
+        const uint32_t tbase = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(acc * kBN);
+#pragma unroll 1
+        for (int ch = 0; ch < kBN / 32; ++ch) {
+            const int col0 = tk.nb * kBN + ch * 32;
+            uint32_t r[32];
+            tmem_ld32(tbase + ch * 32, r);
+            tmem_wait_ld();
+            if (!valid || col0 >= ncols) continue;
+            float v[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __fadd_rn(__uint_as_float(r[i]), __ldg(bias + ch * 32 + i));
+            if (tk.type == 0) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = activation(P.act, v[i]);
+                if (PREC == kFP32) {
+                    float4* hi = reinterpret_cast<float4*>(reinterpret_cast<float*>(R.c1[0]) + grow * P.D + col0);
+                    float4* lo = reinterpret_cast<float4*>(reinterpret_cast<float*>(R.c1[1]) + grow * P.D + col0);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        float4 h, l;
+                        h.x = tf32_hi(v[4 * i]); h.y = tf32_hi(v[4 * i + 1]);
+                        h.z = tf32_hi(v[4 * i + 2]); h.w = tf32_hi(v[4 * i + 3]);
+                        l.x = __fsub_rn(v[4 * i], h.x); l.y = __fsub_rn(v[4 * i + 1], h.y);
+                        l.z = __fsub_rn(v[4 * i + 2], h.z); l.w = __fsub_rn(v[4 * i + 3], h.w);
+                        hi[i] = h;
+                        lo[i] = l;
+                    }
+                } else {
+                    uint4* d = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(R.c1[0]) + grow * P.D + col0);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        uint4 o;
+                        __nv_bfloat162 p0 = __floats2bfloat162_rn(v[8 * i + 0], v[8 * i + 1]);
+                        __nv_bfloat162 p1 = __floats2bfloat162_rn(v[8 * i + 2], v[8 * i + 3]);
+                        __nv_bfloat162 p2 = __floats2bfloat162_rn(v[8 * i + 4], v[8 * i + 5]);
+                        __nv_bfloat162 p3 = __floats2bfloat162_rn(v[8 * i + 6], v[8 * i + 7]);
+                        o.x = *reinterpret_cast<uint32_t*>(&p0);
+                        o.y = *reinterpret_cast<uint32_t*>(&p1);
+                        o.z = *reinterpret_cast<uint32_t*>(&p2);
+                        o.w = *reinterpret_cast<uint32_t*>(&p3);
+                        d[i] = o;
+                    }
+                }
+            } else {
+                float4* d = reinterpret_cast<float4*>(ydst + ch * 32);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) d[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            }
+        }
+        tc_fence_before();
+        asm volatile("bar.sync 1, 128;" ::: "memory");   // all epilogue rows stored, TMEM drained
+        if (et == 0) {
+            mbar_arrive(&G.tempty[acc]);
+            if (tk.type == 0) {
+                __threadfence();
+                atomicAdd(R.g0done + (size_t)tk.le * P.MT + tk.m, 1u);
+                stat[0]++;
+            } else {
+                __threadfence_system();
+                const int rbf = P.Cp >= kBM ? (tk.m % (P.Cp / kBM)) : 0;
+                for (int j = 0; j < tk.nsrc; ++j) {
+                    if (tk.cnt[j] <= 0) continue;
+                    unsigned long long* f = reinterpret_cast<unsigned long long*>(R.peer_heap[tk.src0 + j] +
+                                                                                  R.hl.cflag[par]) +
+                                            ((size_t)e_glob * P.RBF + rbf) * P.NB1 + tk.nb;
+                    st_release_sys(f, ((uint64_t)P.epoch << 32) | (uint32_t)tk.cnt[j]);
+                }
+                stat[1]++;
+            }
+            mbar_arrive(&G.qempty[q]);
+        }
+        if (++q == kTaskRing) { q = 0; qphase ^= 1u; }
+        if (++acc == kAccStages) { acc = 0; aphase ^= 1u; }
+    }
+}
+
+// ================================================================ phase 4: combine
+__device__ void combine_phase(const LaunchParams& P, const RankCtx& R, float* __restrict__ O, uint8_t* smem,
+                              unsigned long long* stat) {
+    const int S = P.S, H = P.H, K = P.k;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t par = P.epoch & 1u;
+    int* sTask = reinterpret_cast<int*>(smem);
+    const int ntask = (S + kCombineTok - 1) / kCombineTok;
+    const float* yc = reinterpret_cast<const float*>(R.peer_heap[R.rank] + R.hl.yc);
+    const unsigned long long* cflag =
+        reinterpret_cast<const unsigned long long*>(R.peer_heap[R.rank] + R.hl.cflag[par]);
+    while (true) {
+        __syncthreads();
+        if (tid == 0) sTask[0] = ld_volatile_u32(P.abort_flag) ? ntask : (int)atomicAdd(R.comb_head, 1u);
+        __syncthreads();
+        const int t = sTask[0];
+        if (t >= ntask) break;
+        if (tid == 0) stat[2]++;
+        for (int i = warp; i < kCombineTok; i += kThreads / 32) {
+            const int tok = t * kCombineTok + i;
+            if (tok >= S) break;
+            // wait for every combine tile this token needs (lanes poll column blocks)
+            bool ok = true;
+            for (int j = 0; j < K && ok; ++j) {
+                const int slot = R.pick_slot[(size_t)tok * K + j];
+                if (slot < 0) continue;
+                const int e = R.pick_e[(size_t)tok * K + j];
+                const int rbf = P.Cp >= kBM ? slot / kBM : 0;
+                for (int nb = lane; nb < P.NB1; nb += 32)
+                    if (wait_epoch_flag(P, R, cflag + ((size_t)e * P.RBF + rbf) * P.NB1 + nb, 400) < 0) ok = false;
+            }
+            if (!__all_sync(0xffffffffu, ok)) break;   // aborted: the next task fetch sees the abort word
+            __syncwarp();   // other lanes' acquires order this lane's reads of the landed rows
+            float4* orow = reinterpret_cast<float4*>(O + (size_t)tok * H);
+            for (int c = lane; c < (H >> 2); c += 32) {
+                float4 acc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                for (int j = 0; j < K; ++j) {
+                    const int slot = R.pick_slot[(size_t)tok * K + j];
+                    if (slot < 0) continue;   // capacity-dropped: zero contribution
+                    const int e = R.pick_e[(size_t)tok * K + j];
+                    const float w = R.pick_w[(size_t)tok * K + j];
+                    const float4 y = *(reinterpret_cast<const float4*>(yc + ((size_t)e * P.C + slot) * H) + c);
+                    acc.x = __fadd_rn(acc.x, __fmul_rn(w, y.x));
+                    acc.y = __fadd_rn(acc.y, __fmul_rn(w, y.y));
+                    acc.z = __fadd_rn(acc.z, __fmul_rn(w, y.z));
+                    acc.w = __fadd_rn(acc.w, __fmul_rn(w, y.w));
+                }
+                orow[c] = acc;
+            }
+        }
+    }
+}
+
+// ================================================================ the layer kernel
+template <int PREC>
+__global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_constant__ LaunchParams P) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    using Cfg = GemmCfg<PREC>;
+    const int rl = blockIdx.x / P.ctas_per_rank;
+    const int cta = blockIdx.x % P.ctas_per_rank;
+    const RankCtx& R = P.ranks[rl];
+    const float* A = P.in[rl];
+    float* O = P.out[rl];
+    const int tid = threadIdx.x, warp = tid >> 5;
+    __shared__ unsigned long long s_stat[4];
+    if (tid < 4) s_stat[tid] = 0;
+
+    GemmCtrl& G = *reinterpret_cast<GemmCtrl*>(smem + Cfg::RING_BYTES);
+    uint8_t* ring = smem;
+
+    // TMEM: allocated once for the whole launch (1 CTA per SM, all 512 columns)
+    if (warp == 2) {
+        tmem_alloc(&G.tmem_base, 512);
+        tmem_relinquish();
+    }
+    // phase 0: rank-local control reset (consumed only after the grid barrier)
+    if (cta == 0) {
+        if (tid == 0) { *R.gemm_head = 0; *R.comb_head = 0; }
+        for (int e = tid; e < P.E; e += kThreads) R.sent[e] = 0;
+        for (int i = tid; i < P.El * P.MT; i += kThreads) R.g0done[i] = 0;
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = G.tmem_base;
+
+    // phase 1: exact gate (uses the smem ring as scratch)
+    gate_phase(P, R, A, cta, smem);
+    if (!rank_barrier(P, R, P.launch_seq)) goto done;
+
+    // phase 2: slot assignment + dispatch
+    dispatch_phase(P, R, A, cta, smem);
+    __syncthreads();
+
+    // phase 3: expert FFN tiles
+    if (tid == 0) {
+        for (int i = 0; i < Cfg::STAGES; ++i) { mbar_init(&G.full[i], 1); mbar_init(&G.empty[i], 1); }
+        for (int i = 0; i < kAccStages; ++i) { mbar_init(&G.tfull[i], 1); mbar_init(&G.tempty[i], 1); }
+        for (int i = 0; i < kTaskRing; ++i) { mbar_init(&G.qfull[i], 1); mbar_init(&G.qempty[i], 2); }
+        G.tmem_base = tmem_base;
+        mbar_fence_init();
+    }
+    fence_proxy_async_smem();   // smem ring was written by the generic proxy in phases 1-2
+    __syncthreads();
+    if (warp == 0) {
+        if ((tid & 31) == 0) gemm_producer<PREC>(P, R, ring, G);
+    } else if (warp == 1) {
+        if ((tid & 31) == 0) gemm_mma<PREC>(P, ring, G);
+    } else if (warp >= 4) {
+        gemm_epilogue<PREC>(P, R, G, s_stat);
+    }
+    __syncthreads();
+
+    // phase 4: combine
+    if (ld_volatile_u32(P.abort_flag) == 0) combine_phase(P, R, O, smem, s_stat);
+
+done:
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, 512);
+    }
+    if (tid == 0) {
+        atomicAdd(R.stats + 0, s_stat[0]);
+        atomicAdd(R.stats + 1, s_stat[1]);
+        atomicAdd(R.stats + 2, s_stat[2]);
+    }
+}
+
+// ================================================================ weight preparation
+// W (E_local x R x Cc, row-major, the reference's N-contiguous layout) ->
+// W^T (E_local x Cc x R, K-major) as tf32 hi/lo planes or bf16.
+__global__ void prep_transpose_kernel(const float* __restrict__ W, int El, int Rr, int Cc, void* out_hi,
+                                      void* out_lo, int prec) {
+    __shared__ float tile[32][33];
+    const int e = blockIdx.z;
+    const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+    const float* src = W + (size_t)e * Rr * Cc;
+    for (int i = threadIdx.y; i < 32; i += 8) {
+        const int r = r0 + i, c = c0 + threadIdx.x;
+        tile[i][threadIdx.x] = (r < Rr && c < Cc) ? src[(size_t)r * Cc + c] : 0.0f;
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += 8) {
+        const int c = c0 + i, r = r0 + threadIdx.x;   // output row c, col r
+        if (c < Cc && r < Rr) {
+            const float v = tile[threadIdx.x][i];
+            const size_t o = (size_t)e * Cc * Rr + (size_t)c * Rr + r;
+            if (prec == kFP32) {
+                const float h = tf32_hi(v);
+                reinterpret_cast<float*>(out_hi)[o] = h;
+                reinterpret_cast<float*>(out_lo)[o] = __fsub_rn(v, h);
+            } else {
+                reinterpret_cast<__nv_bfloat16*>(out_hi)[o] = __float2bfloat16_rn(v);
+            }
+        }
+    }
+}
+
+// ================================================================ debug entry points
+__global__ void debug_expf_kernel(const float* x, float* y, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        y[i] = expf_glibc(x[i]);
+}
+
+// Single-tile GEMM through the same TMA -> tcgen05 -> TMEM path (tests the descriptors):
+// D[128 x 256] = A[128 x K] * B[256 x K]^T with A/B given as K-major tensor maps.
+template <int PREC>
+__global__ void __launch_bounds__(kThreads, 1) debug_gemm_kernel(const __grid_constant__ CUtensorMap ta0,
+                                                                 const __grid_constant__ CUtensorMap ta1,
+                                                                 const __grid_constant__ CUtensorMap tb0,
+                                                                 const __grid_constant__ CUtensorMap tb1, int K,
+                                                                 float* D, uint32_t* abort_flag) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    using Cfg = GemmCfg<PREC>;
+    GemmCtrl& G = *reinterpret_cast<GemmCtrl*>(smem + Cfg::RING_BYTES);
+    const int tid = threadIdx.x, warp = tid >> 5;
+    if (warp == 2) { tmem_alloc(&G.tmem_base, 512); tmem_relinquish(); }
+    if (tid == 0) {
+        for (int i = 0; i < Cfg::STAGES; ++i) { mbar_init(&G.full[i], 1); mbar_init(&G.empty[i], 1); }
+        mbar_init(&G.tfull[0], 1);
+        mbar_fence_init();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = G.tmem_base;
+    const int nk = (K + Cfg::BK - 1) / Cfg::BK;
+    if (tid == 0) {
+        int stage = 0; uint32_t phase = 0;
+        const CUtensorMap* ta[2] = {&ta0, &ta1};
+        const CUtensorMap* tb[2] = {&tb0, &tb1};
+        for (int kb = 0; kb < nk; ++kb) {
+            mbar_wait(&G.empty[stage], phase ^ 1u, abort_flag);
+            uint8_t* st = smem + stage * Cfg::STAGE_BYTES;
+            mbar_expect_tx(&G.full[stage], Cfg::STAGE_BYTES);
+            for (int pl = 0; pl < Cfg::PLANES; ++pl) {
+                tma_load_2d(st + pl * Cfg::A_BYTES, ta[pl], &G.full[stage], kb * Cfg::BK, 0);
+                tma_load_2d(st + Cfg::PLANES * Cfg::A_BYTES + pl * Cfg::B_BYTES, tb[pl], &G.full[stage], kb * Cfg::BK, 0);
+            }
+            if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
+        }
+    } else if (tid == 32) {
+        int stage = 0; uint32_t phase = 0;
+        for (int kb = 0; kb < nk; ++kb) {
+            mbar_wait(&G.full[stage], phase, abort_flag);
+            tc_fence_after();
+            const uint32_t base = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+            for (int ks = 0; ks < Cfg::BK / Cfg::KSTEP; ++ks) {
+                const uint32_t koff = ks * Cfg::KSTEP * Cfg::ESZ;
+                const uint64_t a0 = umma_desc_kmajor(base + koff, 128);
+                const uint64_t b0 = umma_desc_kmajor(base + Cfg::PLANES * Cfg::A_BYTES + koff, 128);
+                const uint32_t accum = (kb | ks) != 0 ? 1u : 0u;
+                if (PREC == kFP32) {
+                    const uint64_t a1 = umma_desc_kmajor(base + Cfg::A_BYTES + koff, 128);
+                    const uint64_t b1 = umma_desc_kmajor(base + Cfg::PLANES * Cfg::A_BYTES + Cfg::B_BYTES + koff, 128);
+                    mma_tf32(tmem, a1, b0, Cfg::IDESC, accum);
+                    mma_tf32(tmem, a0, b1, Cfg::IDESC, 1u);
+                    mma_tf32(tmem, a0, b0, Cfg::IDESC, 1u);
+                } else {
+                    mma_bf16(tmem, a0, b0, Cfg::IDESC, accum);
+                }
+            }
+            mma_commit(&G.empty[stage]);
+            if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
+        }
+        mma_commit(&G.tfull[0]);
+    }
+    if (warp >= 4) {
+        const int et = tid - 128, wq = et >> 5;
+        mbar_wait(&G.tfull[0], 0, abort_flag);
+        tc_fence_after();
+        for (int ch = 0; ch < kBN / 32; ++ch) {
+            uint32_t r[32];
+            tmem_ld32(tmem + ((uint32_t)(wq * 32) << 16) + ch * 32, r);
+            tmem_wait_ld();
+            for (int i = 0; i < 32; ++i) D[(size_t)et * kBN + ch * 32 + i] = __uint_as_float(r[i]);
+        }
+        tc_fence_before();
+    }
+    __syncthreads();
+    if (warp == 2) { tc_fence_after(); tmem_dealloc(tmem, 512); }
+}
+
+// ---------------------------------------------------------------- host-visible launchers
+int layer_smem_bytes(int prec) {
+    const int g = prec == kFP32 ? GemmCfg<kFP32>::SMEM_BYTES : GemmCfg<kBF16>::SMEM_BYTES;
+    return g + 1024;   // + alignment slack
+}
+
+cudaError_t launch_layer(const LaunchParams& p, int grid, int smem, cudaStream_t stream) {
+    void* args[] = {const_cast<LaunchParams*>(&p)};
+    if (p.prec == kFP32) {
+        cudaFuncSetAttribute(fdmoe_layer_kernel<kFP32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        return cudaLaunchCooperativeKernel((const void*)fdmoe_layer_kernel<kFP32>, dim3(grid), dim3(kThreads), args,
+                                           (size_t)smem, stream);
+    }
+    cudaFuncSetAttribute(fdmoe_layer_kernel<kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    return cudaLaunchCooperativeKernel((const void*)fdmoe_layer_kernel<kBF16>, dim3(grid), dim3(kThreads), args,
+                                       (size_t)smem, stream);
+}
+
+int layer_max_blocks_per_sm(int prec, int smem) {
+    int n = 0;
+    if (prec == kFP32) {
+        cudaFuncSetAttribute(fdmoe_layer_kernel<kFP32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fdmoe_layer_kernel<kFP32>, kThreads, smem);
+    } else {
+        cudaFuncSetAttribute(fdmoe_layer_kernel<kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fdmoe_layer_kernel<kBF16>, kThreads, smem);
+    }
+    return n;
+}
+
+cudaError_t launch_prep_transpose(const float* W, int El, int Rr, int Cc, void* hi, void* lo, int prec,
+                                  cudaStream_t s) {
+    dim3 grid((Cc + 31) / 32, (Rr + 31) / 32, El);
+    prep_transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(W, El, Rr, Cc, hi, lo, prec);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_debug_expf(const float* x, float* y, long long n, cudaStream_t s) {
+    debug_expf_kernel<<<1024, 256, 0, s>>>(x, y, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_debug_gemm(int prec, const CUtensorMap* t, int K, float* D, uint32_t* abort_flag, cudaStream_t s) {
+    const int smem = layer_smem_bytes(prec);
+    if (prec == kFP32) {
+        cudaFuncSetAttribute(debug_gemm_kernel<kFP32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        debug_gemm_kernel<kFP32><<<1, kThreads, smem, s>>>(t[0], t[1], t[2], t[3], K, D, abort_flag);
+    } else {
+        cudaFuncSetAttribute(debug_gemm_kernel<kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        debug_gemm_kernel<kBF16><<<1, kThreads, smem, s>>>(t[0], t[1], t[2], t[3], K, D, abort_flag);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace fdmoe

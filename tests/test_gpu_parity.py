@@ -1,0 +1,133 @@
+"""GPU parity: the CUDA operator (through the C ABI) against the CPU oracle on identical inputs.
+
+Bar (BASELINE.json north_star): routing — expert assignment, token-to-slot indices, capacity
+drops, G_phi and combine weights — bit-exact; outputs within 1e-4 relative (normwise,
+harness.hpp:163-175) and 1e-5 absolute + 1e-4 relative per element in FP32 (3xTF32) mode;
+1e-2 relative (normwise) in bf16 mode.
+"""
+import numpy as np
+import pytest
+
+import paper_2506_04667_b200 as fd
+from oracle import pyoracle as po
+
+pytestmark = pytest.mark.gpu
+
+FP32_REL = 1e-4     # normwise, harness.hpp:163-175
+FP32_ATOL = 1e-5    # elementwise: |got - want| <= FP32_ATOL + FP32_REL * |want|
+BF16_REL = 1e-2
+
+
+def _check_routing(cfg, shard, model, gate):
+    cap = fd.expert_capacity(cfg)
+    want = po.gate(shard, model.wg, cfg.topk, cap)
+    assert np.array_equal(gate.g_phi.view(np.uint32), want["g_phi"].view(np.uint32)), "G_phi not bit-exact"
+    assert np.array_equal(gate.slot_counts, want["slot_counts"]), "slot counts differ"
+    assert np.array_equal(gate.table_token, want["table_token"][:, :cap]), "T_phi token indices differ"
+    assert np.array_equal(gate.table_weight.view(np.uint32), want["table_weight"][:, :cap].view(np.uint32)), \
+        "T_phi combine weights not bit-exact"
+    assert gate.dropped == want["dropped"], "capacity drops differ"
+    assert np.array_equal(gate.picks_expert, want["picks_expert"])
+    assert np.array_equal(gate.picks_slot, want["picks_slot"])
+
+
+def _check_outputs(cfg, got, want):
+    rel = fd.max_rel_error([got], [want])
+    tol = FP32_REL if cfg.precision == fd.Precision.fp32 else BF16_REL
+    assert rel <= tol, f"normwise relative error {rel:.3e} > {tol}"
+    if cfg.precision == fd.Precision.fp32:
+        err = np.abs(got.astype(np.float64) - want.astype(np.float64))
+        bound = FP32_ATOL + FP32_REL * np.abs(want.astype(np.float64))
+        bad = int(np.sum(err > bound))
+        assert bad == 0, f"{bad} elements outside {FP32_ATOL} + {FP32_REL}*|want| (max err {err.max():.3e})"
+    # dropped-everything rows are exactly zero
+    return rel
+
+
+def test_device_expf_matches_glibc():
+    rng = np.random.default_rng(0)
+    x = np.concatenate([
+        -rng.random(4_000_000, dtype=np.float32) * 110.0,
+        -rng.random(1_000_000, dtype=np.float32) * 1e-3,
+        np.array([0.0, -0.0, -1e-45, -87.3, -88.0, -88.72, -103.9, -103.97, -104.0, -150.0, -np.inf], np.float32),
+    ]).astype(np.float32)
+    y = np.empty_like(x)
+    fd._check(fd.lib().fdmoe_debug_expf(fd._ptr(x), fd._ptr(y), x.size))
+    want = po.expf_libm(x)
+    mism = np.nonzero(y.view(np.uint32) != want.view(np.uint32))[0]
+    assert mism.size == 0, f"{mism.size} mismatches, first x={x[mism[:3]]}"
+
+
+@pytest.mark.parametrize("prec", [fd.Precision.fp32, fd.Precision.bf16])
+@pytest.mark.parametrize("K", [64, 512])
+def test_tcgen05_tile(prec, K):
+    rng = np.random.default_rng(K + prec)
+    A = rng.standard_normal((128, K)).astype(np.float32)
+    B = rng.standard_normal((256, K)).astype(np.float32)
+    D = np.empty((128, 256), np.float32)
+    fd._check(fd.lib().fdmoe_debug_gemm(prec, K, fd._ptr(A), fd._ptr(B), fd._ptr(D)))
+    if prec == fd.Precision.fp32:
+        want = A.astype(np.float64) @ B.astype(np.float64).T
+        err = np.abs(D - want).max() / np.abs(want).max()
+        assert err < 2e-6, err
+    else:
+        import torch
+        Ab = torch.from_numpy(A).bfloat16().double().numpy()
+        Bb = torch.from_numpy(B).bfloat16().double().numpy()
+        want = Ab @ Bb.T
+        err = np.abs(D - want).max() / np.abs(want).max()
+        assert err < 1e-5, err
+
+
+SINGLE = [
+    # (S, H, D, E, k, cf, act, prec)
+    (256, 128, 256, 8, 2, 1.0, "relu", fd.Precision.fp32),
+    (200, 64, 96, 4, 1, 1.0, "gelu", fd.Precision.fp32),        # ragged tokens / N tile
+    (512, 256, 512, 16, 2, 1.0, "identity", fd.Precision.fp32),
+    (300, 128, 256, 8, 2, 2.0, "relu", fd.Precision.fp32),      # cf > 1: few drops, partial packets
+    (1024, 256, 512, 8, 3, 1.0, "relu", fd.Precision.fp32),     # k = 3, C = 128
+    (512, 256, 512, 16, 2, 1.0, "relu", fd.Precision.bf16),
+]
+
+
+@pytest.mark.parametrize("S,H,D,E,k,cf,act,prec", SINGLE)
+def test_forward_single_rank(S, H, D, E, k, cf, act, prec):
+    cfg = fd.MoeConfig(tokens_per_device=S, embed_dim=H, ffn_dim=D, experts_total=E, devices=1, topk=k,
+                       capacity_factor=cf, activation=fd.Activation.parse(act), precision=prec, seed=3)
+    model = fd.make_model(cfg)
+    shards = fd.make_shards(cfg)
+    res = fd.forward(cfg, shards, model)
+    _check_routing(cfg, shards[0], model, res.gates[0])
+    want = po.dense_forward(shards[0], model, cfg, threads=8)
+    _check_outputs(cfg, res.outputs[0], want)
+    assert res.stats[0].launches == 1
+
+
+@pytest.mark.parametrize("P,E", [(2, 8), (4, 16), (8, 16)])
+def test_forward_virtual_ranks(P, E):
+    """P ranks on one GPU: same single launch, CTAs partitioned by rank; the dispatch and
+    combine exchanges go through each rank's symmetric heap exactly as across GPUs."""
+    cfg = fd.MoeConfig(tokens_per_device=256, embed_dim=128, ffn_dim=256, experts_total=E, devices=P, topk=2,
+                       seed=11)
+    model = fd.make_model(cfg)
+    shards = fd.make_shards(cfg)
+    res = fd.forward(cfg, shards, model)
+    for d in range(P):
+        _check_routing(cfg, shards[d], model, res.gates[d])
+        want = po.dense_forward(shards[d], model, cfg, threads=8)
+        _check_outputs(cfg, res.outputs[d], want)
+
+
+def test_repeated_forward_same_handle():
+    """Epoch-tagged signals: repeated layer calls on one handle need no reset and stay exact."""
+    cfg = fd.MoeConfig(tokens_per_device=256, embed_dim=128, ffn_dim=256, experts_total=8, devices=2, topk=2, seed=5)
+    model = fd.make_model(cfg)
+    op = fd.Operator(cfg)
+    op.set_weights(model)
+    for it in range(4):
+        shards = fd.make_shards(cfg, seed=100 + it)
+        res = op.forward(shards)
+        for d in range(2):
+            _check_routing(cfg, shards[d], model, res.gates[d])
+            _check_outputs(cfg, res.outputs[d], po.dense_forward(shards[d], model, cfg, threads=8))
+    op.close()
