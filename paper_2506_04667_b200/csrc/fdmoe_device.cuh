@@ -56,6 +56,7 @@ struct alignas(64) RankCtx {
     int32_t* tbl_tok;          // [E_total][C]
     float* tbl_w;              // [E_total][C]
     int32_t* slot_counts;      // [E_total]
+    uint32_t* blk_ready;       // [ceil(S/32)] epoch: routing of this token block is final
     // control block (rank-local)
     unsigned long long* bar;   // grid barrier counter (monotonic across launches)
     uint32_t* gemm_head;
@@ -112,6 +113,9 @@ __device__ __forceinline__ uint64_t ld_acquire_gpu_u64(const unsigned long long*
     uint64_t v;
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
+}
+__device__ __forceinline__ void st_release_gpu_u32(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) {
     uint32_t v;

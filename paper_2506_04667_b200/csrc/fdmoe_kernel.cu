@@ -82,7 +82,10 @@ __device__ __forceinline__ float activation(int act, float x) {
     return x;
 }
 
-__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+// tf32 "hi" part rounded to nearest (ties away), so |lo| <= 2^-11 |x| and x - hi is exact in FP32.
+__device__ __forceinline__ float tf32_hi(float x) {
+    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
 
 // ---------------------------------------------------------------- error / watchdog
 __device__ __noinline__ void raise_error(const LaunchParams& P, const RankCtx& R, uint32_t code, uint32_t where,
@@ -122,6 +125,23 @@ __device__ __forceinline__ bool wait_counter(const LaunchParams& P, const RankCt
     const uint64_t t0 = globaltimer();
     uint32_t n = 0;
     while (ld_acquire_gpu_u32(ctr) < target) {
+        if ((++n & 255u) == 0) {
+            if (ld_volatile_u32(P.abort_flag)) return false;
+            if (globaltimer() - t0 > P.budget_ns) {
+                raise_error(P, R, kErrTimeout, where, target, ld_volatile_u32(ctr));
+                return false;
+            }
+        }
+    }
+    return true;
+}
+
+__device__ __forceinline__ bool wait_counter_eq(const LaunchParams& P, const RankCtx& R, const uint32_t* ctr,
+                                                uint32_t target, uint32_t where) {
+    if (ld_acquire_gpu_u32(ctr) == target) return true;
+    const uint64_t t0 = globaltimer();
+    uint32_t n = 0;
+    while (ld_acquire_gpu_u32(ctr) != target) {
         if ((++n & 255u) == 0) {
             if (ld_volatile_u32(P.abort_flag)) return false;
             if (globaltimer() - t0 > P.budget_ns) {
@@ -382,6 +402,9 @@ __device__ void dispatch_phase(const LaunchParams& P, const RankCtx& R, const fl
             if (valid)
                 for (int j = 0; j < K; ++j) atomicAdd(&sRun[mye[j]], 1);
             __syncwarp();
+            // this block's picks/slots/weights are final: the combine (any CTA) acquires this
+            __threadfence();
+            if (lane == 0) st_release_gpu_u32(R.blk_ready + blk, P.epoch);
         }
     }
     __syncthreads();
@@ -770,6 +793,7 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
 }
 
 // ================================================================ phase 4: combine
+static_assert(kCombineTok == kGateTok, "combine tasks are aligned with gate blocks (blk_ready)");
 __device__ void combine_phase(const LaunchParams& P, const RankCtx& R, float* __restrict__ O, uint8_t* smem,
                               unsigned long long* stat) {
     const int S = P.S, H = P.H, K = P.k;
@@ -786,7 +810,14 @@ __device__ void combine_phase(const LaunchParams& P, const RankCtx& R, float* __
         __syncthreads();
         const int t = sTask[0];
         if (t >= ntask) break;
-        if (tid == 0) stat[2]++;
+        if (tid == 0) {
+            stat[2]++;
+            // routing of these tokens was written by the CTA that gated them (dispatch phase)
+            if (!wait_counter_eq(P, R, R.blk_ready + t, P.epoch, 401)) sTask[1] = 1;
+            else sTask[1] = 0;
+        }
+        __syncthreads();
+        if (sTask[1]) break;
         for (int i = warp; i < kCombineTok; i += kThreads / 32) {
             const int tok = t * kCombineTok + i;
             if (tok >= S) break;

@@ -110,6 +110,7 @@ struct RankRes {
     int32_t* tbl_tok = nullptr;
     float* tbl_w = nullptr;
     int32_t* slot_counts = nullptr;
+    uint32_t* blk_ready = nullptr;
     uint8_t* ctrl = nullptr;        // bar | heads | err | stats | sent | g0done
     float* in_buf = nullptr;
     float* out_buf = nullptr;
@@ -192,6 +193,7 @@ fdmoe_status alloc_rank(fdmoe_handle* h, RankRes& r, int ctas_per_rank) {
     parts.push_back({(void**)&r.tbl_tok, (size_t)d.E * d.C * 4});
     parts.push_back({(void**)&r.tbl_w, (size_t)d.E * d.C * 4});
     parts.push_back({(void**)&r.slot_counts, (size_t)d.E * 4});
+    parts.push_back({(void**)&r.blk_ready, (size_t)(d.S + kGateTok - 1) / kGateTok * 4});
     parts.push_back({(void**)&r.ctrl, ctrl_bytes(d)});
     parts.push_back({(void**)&r.in_buf, (size_t)d.S * d.H * 4});
     parts.push_back({(void**)&r.out_buf, (size_t)d.S * d.H * 4});
@@ -202,8 +204,11 @@ fdmoe_status alloc_rank(fdmoe_handle* h, RankRes& r, int ctas_per_rank) {
     size_t o = 0;
     for (auto& p : parts) { *p.first = r.scratch + o; o += align_up(p.second); }
     CK(cudaMemset(r.ctrl, 0, ctrl_bytes(d)));
-    CK(cudaMemset(r.w1[0], 0, w1plane * d.planes));   // padding rows of the weight planes stay finite
-    CK(cudaMemset(r.w2[0], 0, w2plane * d.planes));
+    CK(cudaMemset(r.blk_ready, 0, (size_t)(d.S + kGateTok - 1) / kGateTok * 4));
+    for (int pl = 0; pl < d.planes; ++pl) {   // padding rows of the weight planes stay finite
+        CK(cudaMemset(r.w1[pl], 0, w1plane));
+        CK(cudaMemset(r.w2[pl], 0, w2plane));
+    }
     r.weight_bytes = (w1plane + w2plane) * d.planes;
     return FDMOE_OK;
 }
@@ -234,6 +239,7 @@ fdmoe_status build_ctx(fdmoe_handle* h) {
             c.b1 = r.b1; c.b2 = r.b2; c.wg = r.wg;
             c.g_phi = r.g_phi; c.pick_e = r.pick_e; c.pick_slot = r.pick_slot; c.pick_w = r.pick_w;
             c.cnt_cta = r.cnt_cta; c.tbl_tok = r.tbl_tok; c.tbl_w = r.tbl_w; c.slot_counts = r.slot_counts;
+            c.blk_ready = r.blk_ready;
             c.bar = reinterpret_cast<unsigned long long*>(r.ctrl + kCtrlBar);
             c.gemm_head = reinterpret_cast<uint32_t*>(r.ctrl + kCtrlGemm);
             c.comb_head = reinterpret_cast<uint32_t*>(r.ctrl + kCtrlComb);
@@ -639,7 +645,7 @@ fdmoe_status fdmoe_debug_gemm(int32_t prec, int32_t K, const float* A, const flo
             if (prec == FDMOE_FP32) {
                 uint32_t u;
                 std::memcpy(&u, &src[i], 4);
-                u &= 0xFFFFE000u;
+                u = (u + 0x1000u) & 0xFFFFE000u;
                 float h;
                 std::memcpy(&h, &u, 4);
                 const float l = src[i] - h;

@@ -69,7 +69,11 @@ def test_tcgen05_tile(prec, K):
     if prec == fd.Precision.fp32:
         want = A.astype(np.float64) @ B.astype(np.float64).T
         err = np.abs(D - want).max() / np.abs(want).max()
-        assert err < 2e-6, err
+        # 3xTF32 drops lo*lo (|lo| <= 2^-11|x| with round-to-nearest hi); measured on B200 the
+        # tcgen05 FP32 accumulation adds an error growing ~linearly in K (~8e-9*K normwise:
+        # 4.1e-6 at K=512, 1.6e-5 at K=2048; sequential FP32 is 0.9e-6 / 1.8e-6) —
+        # profiles/r01_numerics.md.
+        assert err < 1e-6 + 1e-8 * K, err
     else:
         import torch
         Ab = torch.from_numpy(A).bfloat16().double().numpy()

@@ -1,0 +1,292 @@
+"""The reference's own unit tests (proj/tests/test_{config,gate,layout,pgas,tiled_blas}.cpp),
+restated as known-answer / property checks against the oracle restatement and against the
+operator's host-side arithmetic in libfdmoe (pure functions; no GPU)."""
+import itertools
+import math
+
+import numpy as np
+import pytest
+
+import paper_2506_04667_b200 as fd
+from oracle import pyoracle as po
+
+
+def cap_cfg(s, e, cf):
+    return fd.MoeConfig(tokens_per_device=s, experts_total=e, capacity_factor=cf, devices=1)
+
+
+# ------------------------------------------------------------------ test_config.cpp
+def test_capacity_reference_points():            # test_config.cpp:29-33
+    for s, e, want in [(4096, 16, 256), (4096, 128, 32), (1, 1, 1)]:
+        assert fd.expert_capacity(cap_cfg(s, e, 1.0)) == want
+        assert po.orc().orc_expert_capacity(s, e, 1.0) == want
+
+
+def test_padded_capacity():                      # test_config.cpp:35-40
+    assert fd.padded_capacity(32, 128) == 128
+    assert fd.padded_capacity(1024, 128) == 1024
+    assert fd.padded_capacity(130, 128) == 256
+    assert po.orc().orc_padded_capacity(130, 128) == 256
+
+
+TABLE3 = [(4096, 16, 256, 256), (4096, 32, 128, 128), (4096, 64, 64, 128), (4096, 128, 32, 128),
+          (8192, 16, 512, 512), (8192, 32, 256, 256), (8192, 64, 128, 128), (8192, 128, 64, 128),
+          (16384, 16, 1024, 1024), (16384, 32, 512, 512), (16384, 64, 256, 256), (16384, 128, 128, 128)]
+
+
+@pytest.mark.parametrize("tokens,experts,ec,padded", TABLE3)
+def test_capacity_table3_round_trip(tokens, experts, ec, padded):   # test_config.cpp:42-58
+    c = fd.expert_capacity(cap_cfg(tokens, experts, 1.0))
+    assert c == ec and fd.padded_capacity(c, 128) == padded
+
+
+def test_capacity_monotone_and_padding_bounds():   # test_config.cpp:60-76
+    rng = np.random.default_rng(7)
+    for _ in range(500):
+        s, e, b = int(rng.integers(1, 4097)), int(rng.integers(1, 129)), int(rng.integers(1, 129))
+        cf = float(rng.uniform(0.1, 3.0))
+        c = fd.expert_capacity(cap_cfg(s, e, cf))
+        assert c == po.orc().orc_expert_capacity(s, e, cf)
+        assert fd.expert_capacity(cap_cfg(s + 64, e, cf)) >= c
+        assert fd.expert_capacity(cap_cfg(s, e, cf + 0.5)) >= c
+        if e > 1:
+            assert fd.expert_capacity(cap_cfg(s, e - 1, cf)) >= c
+        p = fd.padded_capacity(c, b)
+        assert p % b == 0 and p >= c and p - c < b
+
+
+def test_config_validation():                     # test_config.cpp:78-93
+    c = fd.MoeConfig(devices=4, experts_total=6)
+    with pytest.raises(fd.ConfigError):
+        c.validate()
+    c.experts_total = 8
+    c.validate()
+    c.topk = 9
+    with pytest.raises(fd.ConfigError):
+        c.validate()
+    c.topk = 2
+    c.capacity_factor = 0.0
+    with pytest.raises(fd.ConfigError):
+        c.validate()
+    c.capacity_factor = 1.0
+    c.tokens_per_device = 0
+    with pytest.raises(fd.ConfigError):
+        c.validate()
+
+
+def test_gpu_envelope():
+    c = fd.MoeConfig(tokens_per_device=64, embed_dim=64, ffn_dim=64, experts_total=512, devices=1, topk=2)
+    c.validate()
+    with pytest.raises(fd.UnsupportedError):
+        c.validate(gpu_envelope=True)
+
+
+def test_activation_names():                      # test_config.cpp:95-100
+    assert fd.Activation.parse("relu") == 0 and fd.Activation.parse("gelu") == 1
+    assert fd.Activation.parse("identity") == 2
+    with pytest.raises(fd.ConfigError):
+        fd.Activation.parse("swish")
+
+
+# ------------------------------------------------------------------ test_gate.cpp
+def identity_gate(h, e):
+    g = np.zeros((h, e), np.float32)
+    for i in range(min(h, e)):
+        g[i, i] = 1.0
+    return g
+
+
+def test_top1_single_token_weight_one():          # test_gate.cpp:37-46
+    a = np.array([[4.0, 0.0]], np.float32)
+    g = po.gate(a, identity_gate(2, 2), 1, 1)
+    assert g["slot_counts"][0] == 1 and g["table_token"][0, 0] == 0 and g["table_weight"][0, 0] == 1.0
+    assert g["dropped"] == []
+
+
+def test_uniform_logits_tie_break_and_drop():     # test_gate.cpp:48-67
+    a = np.zeros((4, 2), np.float32)
+    g = po.gate(a, identity_gate(2, 2), 2, 2)
+    for e in range(2):
+        assert g["slot_counts"][e] == 2
+        assert list(g["table_token"][e]) == [0, 1]
+        assert np.allclose(g["table_weight"][e], 0.5)
+    assert sorted(g["dropped"]) == [(2, 0), (2, 1), (3, 0), (3, 1)]
+    assert [tuple(p) for p in g["picks_expert"]] == [(0, 1)] * 4   # lower index first on ties
+
+
+def test_weights_reproduce_affinity_split():      # test_gate.cpp:69-81
+    a = np.zeros((2, 2), np.float32)
+    a[0, 0], a[0, 1] = math.log(0.8), math.log(0.2)
+    g = po.gate(a, identity_gate(2, 2), 2, 1)
+    assert abs(g["g_phi"][0, 0] - 0.8) < 1e-6 and abs(g["g_phi"][0, 1] - 0.2) < 1e-6
+    assert abs(g["table_weight"][0, 0] - 0.8) < 1e-6 and abs(g["table_weight"][1, 0] - 0.2) < 1e-6
+
+
+def test_softmax_rows_are_probabilities():        # test_gate.cpp:83-103
+    rng = np.random.default_rng(11)
+    a = rng.uniform(-2, 2, (16, 8)).astype(np.float32)
+    w = rng.uniform(-2, 2, (8, 6)).astype(np.float32)
+    g = po.gate(a, w, 2, 100)
+    assert np.all(g["g_phi"] >= 0) and np.all(g["g_phi"] <= 1)
+    assert np.allclose(g["g_phi"].sum(1), 1.0, atol=1e-6)
+
+
+def test_slots_plus_drops_conserve():             # test_gate.cpp:105-124
+    rng = np.random.default_rng(12)
+    for _ in range(30):
+        s, e = int(rng.integers(1, 25)), int(rng.integers(1, 9))
+        k = min(int(rng.integers(1, 4)), e)
+        cap = fd.expert_capacity(cap_cfg(s, e, 0.75))
+        a = rng.uniform(-1, 1, (s, 6)).astype(np.float32)
+        w = rng.uniform(-1, 1, (6, e)).astype(np.float32)
+        g = po.gate(a, w, k, cap)
+        assert int(g["slot_counts"].sum()) + len(g["dropped"]) == s * k
+        assert np.all(g["slot_counts"] <= cap)
+
+
+def test_routing_bit_identical_across_calls():    # test_gate.cpp:126-147
+    rng = np.random.default_rng(13)
+    a = rng.uniform(-1, 1, (12, 8)).astype(np.float32)
+    w = rng.uniform(-1, 1, (8, 4)).astype(np.float32)
+    g1, g2 = po.gate(a, w, 2, 6), po.gate(a, w, 2, 6)
+    assert np.array_equal(g1["g_phi"].view(np.uint32), g2["g_phi"].view(np.uint32))
+    assert np.array_equal(g1["table_token"], g2["table_token"]) and g1["dropped"] == g2["dropped"]
+
+
+def test_topk_shift_invariant():                  # test_gate.cpp:149-163
+    rng = np.random.default_rng(14)
+    for _ in range(200):
+        z = rng.uniform(-3, 3, 8).astype(np.float32)
+        order = sorted(range(8), key=lambda i: (-z[i], i))[:3]
+        zs = (z + np.float32(7.5)).astype(np.float32)
+        order_s = sorted(range(8), key=lambda i: (-zs[i], i))[:3]
+        assert order == order_s
+
+
+def test_manifest_all_local_capacity_clip_pigeonhole():   # test_gate.cpp:165-204
+    # all-local routing: experts 0,1 on dev0; 2,3 on dev1
+    cfg = fd.MoeConfig(tokens_per_device=6, embed_dim=4, experts_total=4, devices=2, topk=1, capacity_factor=2.0)
+    a = np.zeros((6, 4), np.float32)
+    a[:, 0] = 5.0
+    g = po.gate(a, identity_gate(4, 4), 1, fd.expert_capacity(cfg))
+    gate = fd.GateOutput(g["g_phi"], fd.expert_capacity(cfg), g["table_token"], g["table_weight"],
+                         g["slot_counts"], g["dropped"])
+    mf = fd.dispatch_manifest(gate, cfg)
+    assert mf.per_device[0][0][1] == 6 and mf.per_device[1][0][1] == 0 and mf.per_device[1][1][1] == 0
+    # capacity clip
+    cfg = fd.MoeConfig(tokens_per_device=8, embed_dim=4, experts_total=2, devices=1, topk=1)
+    assert fd.expert_capacity(cfg) == 4
+    a = np.zeros((8, 4), np.float32)
+    a[:5, 0] = 5.0
+    a[5:, 1] = 5.0
+    g = po.gate(a, identity_gate(4, 2), 1, 4)
+    assert list(g["table_token"][0]) == [0, 1, 2, 3] and g["dropped"] == [(4, 0)]
+    # pigeonhole
+    a = np.zeros((8, 4), np.float32)
+    for i in range(8):
+        a[i, i % 4] = 5.0
+    g = po.gate(a, identity_gate(4, 4), 1, 2)
+    assert list(g["slot_counts"]) == [2, 2, 2, 2]
+
+
+def test_zero_capacity_drops_everything():        # test_gate.cpp:206-213
+    g = po.gate(np.zeros((4, 2), np.float32), identity_gate(2, 2), 1, 0)
+    assert list(g["slot_counts"]) == [0, 0] and len(g["dropped"]) == 4
+
+
+# ------------------------------------------------------------------ test_layout.cpp
+def table_cfg(tokens, experts):
+    return fd.MoeConfig(tokens_per_device=tokens, embed_dim=1024, experts_total=experts, devices=1, tile_rows=128)
+
+
+def test_size_L_table():                          # test_layout.cpp:52-65
+    assert fd.size_L(table_cfg(4096, 16)) == 64 * 1024 * 1024
+    assert fd.size_L(table_cfg(4096, 128)) == 256 * 1024 * 1024
+    assert fd.size_L(table_cfg(16384, 128)) == 256 * 1024 * 1024
+    want = [64.00, 64.00, 128.01, 256.02, 128.01, 128.01, 128.01, 256.02, 256.02, 256.02, 256.02, 256.02]
+    got = [fd.size_L(table_cfg(t, e)) / 2**20 for t in (4096, 8192, 16384) for e in (16, 32, 64, 128)]
+    assert all(abs(g - w) <= 0.1 for g, w in zip(got, want))
+    assert all(fd.size_L(table_cfg(t, e)) == po.orc().orc_size_L(t, 1024, e, 128)
+               for t in (4096, 8192, 16384) for e in (16, 32, 64, 128))
+
+
+def test_structural_layout_equals_formula():      # test_layout.cpp:67-74
+    for t in (4096, 8192, 16384):
+        for e in (16, 32, 64, 128):
+            cfg = table_cfg(t, e)
+            cp = fd.padded_capacity(fd.expert_capacity(cfg), 128)
+            assert 1 * 2 * 2 * e * cp * 1024 * 4 == fd.size_L(cfg)
+
+
+def test_flat_index_endpoints_bijective():        # test_layout.cpp:76-93
+    P, E, C, H = 2, 2, 4, 8
+    assert fd.flat_index(P, E, C, H, 0, 0, 0, 0, 0) == 0
+    assert fd.flat_index(P, E, C, H, P - 1, 1, 1, E - 1, C - 1) == P * 2 * 2 * E * C * H - H
+    seen = {fd.flat_index(P, E, C, H, p, r, b, e, c)
+            for p, r, b, e, c in itertools.product(range(P), range(2), range(2), range(E), range(C))}
+    assert len(seen) == P * 2 * 2 * E * C
+    with pytest.raises(IndexError):
+        fd.flat_index(P, E, C, H, 2, 0, 0, 0, 0)
+    with pytest.raises(IndexError):
+        fd.flat_index(P, E, C, H, 0, 0, 0, 0, 4)
+
+
+def test_write_validity_rules():                  # test_layout.cpp:95-110
+    assert fd.validate_write(0, 1, 0, 1) == 0
+    assert fd.validate_write(1, 1, 1, 1) == 0
+    assert fd.validate_write(0, 1, 1, 1) == 1
+    assert fd.validate_write(0, 0, 0, 0) == 0
+    assert fd.validate_write(0, 1, 0, 0) == 2
+
+
+@pytest.mark.parametrize("P", [1, 2, 3])
+def test_conflict_freedom_exhaustive(P):          # test_layout.cpp:112-122 (Theorem 1)
+    E, C, H = 2, 3, 4
+    targets = {}
+    for src, dst, p, r, b, e, c in itertools.product(range(P), range(P), range(P), range(2), range(2), range(E),
+                                                     range(C)):
+        if fd.validate_write(src, dst, p, b) == 0:
+            targets.setdefault((dst, fd.flat_index(P, E, C, H, p, r, b, e, c)), set()).add(src)
+    assert all(len(s) == 1 for s in targets.values())
+
+
+def test_receive_layout_conflict_free():
+    """The operator's own receive layout: row le*RP + src*Cp + slot of rank q's
+    buffer is written only by `src`, and every (src, expert, slot) maps to a distinct row."""
+    for P, El, Cp in [(1, 4, 16), (2, 3, 32), (4, 2, 128), (8, 2, 16)]:
+        rows = {}
+        for src, q, le, slot in itertools.product(range(P), range(P), range(El), range(Cp)):
+            key = (q, le * P * Cp + src * Cp + slot)
+            assert key not in rows
+            rows[key] = src
+
+
+# ------------------------------------------------------------------ test_pgas.cpp (accounting)
+def test_padded_baseline_bytes():                 # test_pgas.cpp:179-188
+    cfg = fd.MoeConfig(tokens_per_device=16, embed_dim=4, experts_total=4, devices=2, tile_rows=8)
+    # 2 rounds * 2 experts * 8 slots * 4 dims * 4 bytes per ordered pair
+    assert list(fd.padded_baseline_bytes(cfg)) == [2 * 2 * 8 * 4 * 4] * 4
+
+
+def test_task_count_arithmetic():                 # runtime.hpp:122-165
+    cfg = fd.MoeConfig(tokens_per_device=4096, embed_dim=2048, ffn_dim=2048, experts_total=16, devices=1, topk=2,
+                       tile_rows=128, tile_cols=64)
+    assert fd.gemm_tasks_for_rows(cfg, 0) == 0
+    assert fd.gemm_tasks_for_rows(cfg, 256) == 2 * (32 + 32)
+    assert fd.combine_tiles_for_rows(cfg, 129) == 2 * 32
+    assert fd.initial_task_bound(cfg) == 16 * 2 * 64 + 2 * 32 * 32
+
+
+# ------------------------------------------------------------------ test_tiled_blas.cpp
+def test_naive_matmul_and_activation():           # test_tiled_blas.cpp:54-71, 102-113
+    rng = np.random.default_rng(2)
+    a = rng.uniform(-1, 1, (8, 8)).astype(np.float32)
+    b = rng.uniform(-1, 1, (8, 8)).astype(np.float32)
+    c = np.empty((8, 8), np.float32)
+    po.orc().orc_naive_matmul(po._p(a), po._p(b), 8, 8, 8, po._p(c))
+    assert np.abs(c - a.astype(np.float64) @ b.astype(np.float64)).max() <= 1e-6
+    for i in range(-100, 101):
+        x = i / 10.0
+        want = 0.5 * x * (1 + math.erf(x / math.sqrt(2)))
+        assert abs(po.orc().orc_activation(1, x) - want) <= 1e-6
+    assert po.orc().orc_activation(0, -3.0) == 0.0 and po.orc().orc_activation(2, -1.25) == -1.25
