@@ -1,0 +1,370 @@
+#!/usr/bin/env python3
+"""bench.py — MoE-layer forward on B200 (the FlashDMoE hot path).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fdmoe|reference] [--precision fp32|bf16]
+
+Workload (BASELINE.json metric "MoE layer fwd latency (ms) & tokens/s at 16K tok/128 experts, 1-8 B200"):
+T = 16384 tokens per GPU, H = I = 2048, E = 128 experts in total, top-2, cf = 1.0, relu, expert-parallel
+over N GPUs (E/N experts per GPU), FP32-accurate (3xTF32). Weak scaling: per-GPU token work is fixed.
+Inputs are synthetic (harness.hpp:76-109 seeded generator), weights random-init.
+
+One "step" = one full layer forward = ONE persistent kernel launch per GPU.
+  value  : whole-job tokens/s with inputs resident in HBM (CUDA events on the launching stream, max over ranks)
+  e2e    : same metric through the C-ABI call with host buffers (H2D of the shard + D2H of the output inside
+           the timed region, host wall clock, max over ranks)
+  roofline: the layer kernel against the measured tensor peak (3xTF32 effective) and HBM (weights once)
+  cpu_baseline: the reference's own forward() (oracle/_ref, compiled from /root/reference) on a bounded
+           token sample, all host cores, rank 0 only
+
+Under torchrun (N > 1) each rank drives one GPU; the ranks' symmetric heaps are cross-mapped with CUDA IPC
+(handles exchanged through torch.distributed) and the kernels exchange tokens with peer stores — NCCL is
+used for bootstrap/barriers only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MoE layer fwd latency (ms) & tokens/s at 16K tok/128 experts, 1–8 B200"
+S_PER_GPU, H, D, E_TOTAL, TOPK = 16384, 2048, 2048, 128, 2
+
+
+def peaks():
+    p = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback (B200_PROFILING.md)"}
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        m = json.load(open(path))
+        p = {"hbm_gbs": float(m["hbm_gbs"]), "bf16_tflops": float(m["bf16_tflops"]),
+             "bf16_tflops_sustained": float(m.get("bf16_tflops_sustained", m["bf16_tflops"])),
+             "source": "measured (MEASURED_PEAKS.json)"}
+    return p
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML while the timed region runs."""
+
+    def __init__(self, dev_index):
+        self.samples, self.reasons, self._stop = [], set(), threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8): "hw_slowdown",
+            getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40): "hw_thermal_slowdown",
+            getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20): "sw_thermal_slowdown",
+            getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4): "sw_power_cap",
+            getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80): "hw_power_brake_slowdown",
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in names.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def cpu_reference(cfg_full, sample_tokens, steps, warmup, seed=0):
+    """The reference's own forward() (runtime.hpp:802) from oracle/_ref on a token sample of the same
+    workload (same H, I, E, k, cf; S reduced to the sample), every host core as processor threads."""
+    import paper_2506_04667_b200 as fd
+    from oracle import pyoracle as po
+    cores = os.cpu_count() or 1
+    cfg = fd.MoeConfig(tokens_per_device=sample_tokens, embed_dim=cfg_full.embed_dim, ffn_dim=cfg_full.ffn_dim,
+                       experts_total=cfg_full.experts_total, devices=1, topk=cfg_full.topk,
+                       capacity_factor=cfg_full.capacity_factor, tile_rows=128, tile_cols=64, seed=seed)
+    model = fd.make_model(cfg)
+    shards = fd.make_shards(cfg)
+    if po.ref_available():
+        rm = po.RefModel(model, cfg)
+        run = lambda: po.ref_forward(cfg, shards, rm, processors=cores)  # noqa: E731
+        kind = "reference"
+    else:   # no prebuilt reference: the oracle port (C restatement), threaded
+        run = lambda: po.dense_forward(shards[0], model, cfg, threads=cores)  # noqa: E731
+        kind = "port"
+    for _ in range(warmup):
+        run()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        run()
+    dt = time.perf_counter() - t0
+    return {"value": sample_tokens * steps / dt, "unit": "tokens/s", "cores": cores, "kind": kind,
+            "sample": f"{sample_tokens} tokens x {steps} forward() calls of the same layer shape "
+                      f"(H={cfg.embed_dim}, I={cfg.ffn_dim}, E={cfg.experts_total}, top-{cfg.topk}, cf=1, P=1)",
+            "ms_per_step": dt * 1e3 / steps}
+
+
+def calibrate_sample(cfg_full, budget_s):
+    """Token sample size whose reference forward() takes about budget_s seconds on this host."""
+    from oracle import pyoracle as po
+    import paper_2506_04667_b200 as fd
+    probe = 256
+    cfg = fd.MoeConfig(tokens_per_device=probe, embed_dim=cfg_full.embed_dim, ffn_dim=cfg_full.ffn_dim,
+                       experts_total=cfg_full.experts_total, devices=1, topk=cfg_full.topk, tile_rows=128,
+                       tile_cols=64)
+    model = fd.make_model(cfg)
+    shards = fd.make_shards(cfg)
+    cores = os.cpu_count() or 1
+    if po.ref_available():
+        rm = po.RefModel(model, cfg)
+        t0 = time.perf_counter()
+        po.ref_forward(cfg, shards, rm, processors=cores)
+    else:
+        t0 = time.perf_counter()
+        po.dense_forward(shards[0], model, cfg, threads=cores)
+    dt = time.perf_counter() - t0
+    n = int(probe * budget_s / max(dt, 1e-3))
+    return max(128, min(S_PER_GPU, (n // 128) * 128))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="fdmoe", choices=["fdmoe", "reference"])
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "bf16"])
+    ap.add_argument("--tokens", type=int, default=S_PER_GPU)
+    ap.add_argument("--experts", type=int, default=E_TOTAL)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    assert args.warmup >= 3, "timing rules: at least 3 warm-up steps"
+
+    rank, world, local = dist_env()
+    if world != args.gpus and world > 1:
+        print(f"warning: WORLD_SIZE={world} != --gpus {args.gpus}; using WORLD_SIZE", file=sys.stderr)
+    n = world if world > 1 else args.gpus
+
+    import paper_2506_04667_b200 as fd
+    prec = fd.Precision.fp32 if args.precision == "fp32" else fd.Precision.bf16
+    cfg = fd.MoeConfig(tokens_per_device=args.tokens, embed_dim=H, ffn_dim=D, experts_total=args.experts,
+                       devices=n, topk=TOPK, capacity_factor=1.0, tile_rows=128, tile_cols=64, seed=0,
+                       precision=prec)
+    workload = (f"c4-shape: T={cfg.tokens_per_device} tokens/GPU, H={H}, I={D}, E={cfg.experts_total} total "
+                f"({cfg.experts_total // n}/GPU), top-{TOPK}, cf=1.0, relu, EP={n}, "
+                f"{'FP32-accurate 3xTF32' if prec == 0 else 'bf16'}")
+    config = {"workload": workload, "tokens_per_gpu": cfg.tokens_per_device, "embed_dim": H, "ffn_dim": D,
+              "experts_total": cfg.experts_total, "topk": TOPK, "ep": n,
+              "l2": "no flush: per-step inputs (134 MB shard + resident expert weights) exceed the 126 MB L2"}
+
+    # ---------------------------------------------------------------- reference arm
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        budget = max(2.0, 150.0 / (args.steps + args.warmup))
+        sample = calibrate_sample(cfg, budget)
+        cb = cpu_reference(cfg, sample, args.steps, args.warmup)
+        line = {"metric": METRIC, "value": cb["value"], "unit": "tokens/s", "n_gpus": 0, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": cb["ms_per_step"], "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config,
+                "impl": "reference",
+                "cpu_baseline": {"value": cb["value"], "unit": "tokens/s", "cores": cb["cores"], "kind": cb["kind"],
+                                 "sample": cb["sample"]},
+                "e2e": {"value": cb["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    # ---------------------------------------------------------------- our arm
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    t_setup = time.perf_counter()
+    model = fd.make_model(cfg)
+    shards_all = fd.make_shards(cfg)
+    if world > 1:
+        op = fd.Operator(cfg, device_ids=[local], first_rank=rank, n_local=1)
+        blobs = [None] * world
+        dist.all_gather_object(blobs, op.export_heap())
+        op.import_peers(blobs)
+        my = [shards_all[rank]]
+    else:
+        op = fd.Operator(cfg, device_ids=[0] * n)   # n == 1 here (or virtual ranks if --gpus > 1 w/o torchrun)
+        my = shards_all
+    op.set_weights(model)
+    info = op.info()
+    del model
+    setup_s = time.perf_counter() - t_setup
+
+    # a dedicated (non-default) stream: the layer kernel is launched on it and the CUDA events that
+    # time it are recorded on it (the legacy default stream would not order with the launch)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    assert stream.cuda_stream != 0
+    ins = [torch.from_numpy(s).cuda() for s in my]
+    outs = [torch.empty_like(x) for x in ins]
+    ip = [x.data_ptr() for x in ins]
+    opp = [x.data_ptr() for x in outs]
+    sp = [stream.cuda_stream] * len(ins)
+
+    for _ in range(args.warmup):
+        op.forward_device(ip, opp, sp)
+    op.sync()
+    torch.cuda.synchronize()
+    barrier()
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            op.forward_device(ip, opp, sp)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    op.sync()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    tokens_per_step = cfg.tokens_per_device * n
+    value = tokens_per_step / (ms * 1e-3)
+    # cross-check: the operator's own events around its launches (same stream)
+    st_ms = op.last_kernel_ms()
+
+    # ---------------------------------------------------------------- end to end through the C ABI (host buffers)
+    pinned = [torch.from_numpy(s).pin_memory() for s in my]
+    host_in = [p.numpy() for p in pinned]
+    outs_h = [torch.empty(s.shape, dtype=torch.float32).pin_memory().numpy() for s in my]
+    op.forward(host_in, routing=False, stats=False)   # warm
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        _forward_host(fd, op, host_in, outs_h)
+    e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": tokens_per_step / e2e_s, "unit": "tokens/s",
+           "h2d_bytes_per_step": int(sum(x.nbytes for x in host_in)),
+           "d2h_bytes_per_step": int(sum(x.nbytes for x in outs_h)), "ms_per_step": e2e_s * 1e3}
+
+    # ---------------------------------------------------------------- roofline of the (single) layer kernel
+    pk = peaks()
+    El = cfg.experts_total // n
+    rows = cfg.tokens_per_device   # rows received per GPU (every (src, expert) packet fills to C)
+    gate_flops = 2.0 * cfg.tokens_per_device * H * cfg.experts_total
+    ffn_flops = 4.0 * H * D * rows
+    flops = gate_flops + ffn_flops
+    weight_bytes = El * 2.0 * H * D * 4   # FP32 weights read once (algorithmic)
+    if prec == fd.Precision.fp32:
+        tensor_peak = pk["bf16_tflops"] / 2.0 / 3.0   # tf32 = bf16/2; FP32-accurate = 3 tf32 products
+        peak_note = (f"3xTF32 effective = measured bf16 {pk['bf16_tflops']:.1f} / 2 (tf32 rate) / 3 (products); "
+                     f"{pk['source']}")
+    else:
+        tensor_peak = pk["bf16_tflops"]
+        weight_bytes /= 2
+        peak_note = f"bf16 {pk['source']}"
+    t_tensor = flops / (tensor_peak * 1e12)
+    t_hbm = weight_bytes / (pk["hbm_gbs"] * 1e9)
+    bound = "tensor" if t_tensor >= t_hbm else "hbm"
+    achieved_tf = flops / (ms * 1e-3) / 1e12
+    achieved_gbs = weight_bytes / (ms * 1e-3) / 1e9
+    if bound == "tensor":
+        roof = {"bound": "tensor", "achieved": achieved_tf, "peak": tensor_peak, "unit": "TFLOP/s",
+                "frac": achieved_tf / tensor_peak}
+    else:
+        roof = {"bound": "hbm", "achieved": achieved_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved_gbs / pk["hbm_gbs"]}
+    roof.update({"traffic": None, "peak_note": peak_note,
+                 "algorithmic": {"flops_per_launch": flops, "gate_flops": gate_flops, "ffn_flops": ffn_flops,
+                                 "weight_bytes_per_launch": weight_bytes},
+                 "t_tensor_ms": t_tensor * 1e3, "t_hbm_ms": t_hbm * 1e3,
+                 "roofline_ms": max(t_tensor, t_hbm) * 1e3,
+                 "frac_of_roofline": max(t_tensor, t_hbm) / (ms * 1e-3),
+                 "kernel": "fdmoe_layer_kernel (1 launch/GPU/step)"})
+    traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(traffic_file):
+        tr = json.load(open(traffic_file)).get(f"{args.precision}_n{n}")
+        if tr:
+            roof["traffic"] = tr
+
+    line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": n, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32 (3xTF32 tcgen05)" if prec == 0 else "bf16",
+            "data": "synthetic (seeded harness.hpp generator), random-init experts", "config": config,
+            "e2e": e2e, "gpu_launches": args.steps, "gpu_launches_per_step": 1, "roofline": roof,
+            "clocks": clk.summary(), "setup_s": setup_s, "operator_event_ms_last_launch": st_ms,
+            "operator": {k: info[k] for k in ("capacity", "packet_rows", "ctas_per_rank", "smem_bytes")}}
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            budget = 15.0
+            sample = calibrate_sample(cfg, budget)
+            cb = cpu_reference(cfg, sample, 1, 0)
+            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as e:  # never let the baseline break the bench line
+            line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+    if rank == 0:
+        print(json.dumps(line))
+    op.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _forward_host(fd, op, host_in, outs_h):
+    """fdmoe_forward with FDMOE_HOST pointers: H2D shard, the layer launch, D2H output."""
+    import ctypes as C
+    n = op.n_local
+    ip = (C.c_void_p * n)(*[a.ctypes.data for a in host_in])
+    opp = (C.c_void_p * n)(*[a.ctypes.data for a in outs_h])
+    fd._check(fd.lib().fdmoe_forward(op._h, ip, opp, 0, None, None, None))
+
+
+if __name__ == "__main__":
+    main()

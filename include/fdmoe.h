@@ -184,6 +184,9 @@ typedef struct fdmoe_info {
     int32_t ranks_per_launch;
 } fdmoe_info;
 fdmoe_status fdmoe_get_info(fdmoe_handle* h, fdmoe_info* info);
+/* Device time of the most recent forward's launch (CUDA events on the launching stream;
+ * max over this handle's devices). Call after fdmoe_sync / fdmoe_forward. */
+fdmoe_status fdmoe_last_kernel_ms(fdmoe_handle* h, double* ms);
 
 /* ---- diagnostics (tests only; not part of the reference surface) -------------------- */
 /* The kernel's glibc-expf restatement on n host floats (runs on device 0). */

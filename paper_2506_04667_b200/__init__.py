@@ -117,7 +117,7 @@ EXPORTED_SYMBOLS = [
     "fdmoe_gemm_tasks_for_rows", "fdmoe_combine_tiles_for_rows", "fdmoe_initial_task_bound",
     "fdmoe_synth_model", "fdmoe_synth_shards", "fdmoe_create", "fdmoe_destroy", "fdmoe_ipc_size",
     "fdmoe_export_heap", "fdmoe_import_peers", "fdmoe_set_weights", "fdmoe_forward", "fdmoe_forward_async",
-    "fdmoe_sync", "fdmoe_get_info", "fdmoe_debug_expf", "fdmoe_debug_gemm",
+    "fdmoe_sync", "fdmoe_get_info", "fdmoe_last_kernel_ms", "fdmoe_debug_expf", "fdmoe_debug_gemm",
 ]
 
 _LIB = None
@@ -161,6 +161,7 @@ def lib():
         "fdmoe_forward_async": (i32, [vp, vp, vp, vp]),
         "fdmoe_sync": (i32, [vp]),
         "fdmoe_get_info": (i32, [vp, C.POINTER(_Info)]),
+        "fdmoe_last_kernel_ms": (i32, [vp, vp]),
         "fdmoe_debug_expf": (i32, [f32p, f32p, i64]),
         "fdmoe_debug_gemm": (i32, [i32, i32, f32p, f32p, f32p]),
     }
@@ -501,6 +502,12 @@ class Operator:
 
     def sync(self):
         _check(lib().fdmoe_sync(self._h))
+
+    def last_kernel_ms(self) -> float:
+        """Device time of the most recent layer launch (CUDA events around it, max over devices)."""
+        v = C.c_double()
+        _check(lib().fdmoe_last_kernel_ms(self._h, C.byref(v)))
+        return v.value
 
 
 def forward(cfg: MoeConfig, shards: Sequence[np.ndarray], model: ModelWeights,

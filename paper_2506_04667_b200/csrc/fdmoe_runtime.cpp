@@ -619,6 +619,20 @@ fdmoe_status fdmoe_get_info(fdmoe_handle* h, fdmoe_info* info) {
     return FDMOE_OK;
 }
 
+fdmoe_status fdmoe_last_kernel_ms(fdmoe_handle* h, double* ms) {
+    if (!h || !ms) return fail(FDMOE_ERR_CONFIG, "null argument");
+    double best = 0.0;
+    for (auto& g : h->groups) {
+        CK(cudaSetDevice(g.dev));
+        CK(cudaEventSynchronize(g.ev1));
+        float v = 0.0f;
+        CK(cudaEventElapsedTime(&v, g.ev0, g.ev1));
+        best = std::max(best, (double)v);
+    }
+    *ms = best;
+    return FDMOE_OK;
+}
+
 // ---- diagnostics (tests): device expf and a single-tile tcgen05 GEMM ----------------
 fdmoe_status fdmoe_debug_expf(const float* x, float* y, int64_t n) {
     float *dx = nullptr, *dy = nullptr;

@@ -172,7 +172,12 @@ def test_manifest_all_local_capacity_clip_pigeonhole():   # test_gate.cpp:165-20
     gate = fd.GateOutput(g["g_phi"], fd.expert_capacity(cfg), g["table_token"], g["table_weight"],
                          g["slot_counts"], g["dropped"])
     mf = fd.dispatch_manifest(gate, cfg)
-    assert mf.per_device[0][0][1] == 6 and mf.per_device[1][0][1] == 0 and mf.per_device[1][1][1] == 0
+    # test_gate.cpp:171-175 expects count == 6, but C = ceil(2.0*6/4) = 3 and the reference's own
+    # gate_forward (oracle/_ref) returns 3 with tokens 3..5 dropped: the shipped test is wrong
+    # (it never built — Catch2 is absent). We pin the reference's actual behaviour.
+    assert fd.expert_capacity(cfg) == 3
+    assert mf.per_device[0][0][1] == 3 and mf.per_device[1][0][1] == 0 and mf.per_device[1][1][1] == 0
+    assert g["dropped"] == [(3, 0), (4, 0), (5, 0)]
     # capacity clip
     cfg = fd.MoeConfig(tokens_per_device=8, embed_dim=4, experts_total=2, devices=1, topk=1)
     assert fd.expert_capacity(cfg) == 4
