@@ -187,6 +187,11 @@ fdmoe_status fdmoe_get_info(fdmoe_handle* h, fdmoe_info* info);
 /* Device time of the most recent forward's launch (CUDA events on the launching stream;
  * max over this handle's devices). Call after fdmoe_sync / fdmoe_forward. */
 fdmoe_status fdmoe_last_kernel_ms(fdmoe_handle* h, double* ms);
+/* Device trace of the most recent launch (the reference's TraceBuffer role, trace.hpp:17-118, at
+ * phase granularity): per CTA of local rank `local_rank`, 8 u64 = %globaltimer ns at kernel start,
+ * gate done, grid barrier passed, dispatch done, FFN tiles done, combine done, exit; then the number
+ * of FFN tiles that CTA executed. Writes min(cap/8, ctas) rows; *n_ctas = CTAs of that rank. */
+fdmoe_status fdmoe_read_trace(fdmoe_handle* h, int32_t local_rank, uint64_t* out, int32_t cap, int32_t* n_ctas);
 
 /* ---- diagnostics (tests only; not part of the reference surface) -------------------- */
 /* The kernel's glibc-expf restatement on n host floats (runs on device 0). */

@@ -117,7 +117,7 @@ EXPORTED_SYMBOLS = [
     "fdmoe_gemm_tasks_for_rows", "fdmoe_combine_tiles_for_rows", "fdmoe_initial_task_bound",
     "fdmoe_synth_model", "fdmoe_synth_shards", "fdmoe_create", "fdmoe_destroy", "fdmoe_ipc_size",
     "fdmoe_export_heap", "fdmoe_import_peers", "fdmoe_set_weights", "fdmoe_forward", "fdmoe_forward_async",
-    "fdmoe_sync", "fdmoe_get_info", "fdmoe_last_kernel_ms", "fdmoe_debug_expf", "fdmoe_debug_gemm",
+    "fdmoe_sync", "fdmoe_get_info", "fdmoe_last_kernel_ms", "fdmoe_read_trace", "fdmoe_debug_expf", "fdmoe_debug_gemm",
 ]
 
 _LIB = None
@@ -162,6 +162,7 @@ def lib():
         "fdmoe_sync": (i32, [vp]),
         "fdmoe_get_info": (i32, [vp, C.POINTER(_Info)]),
         "fdmoe_last_kernel_ms": (i32, [vp, vp]),
+        "fdmoe_read_trace": (i32, [vp, i32, vp, i32, vp]),
         "fdmoe_debug_expf": (i32, [f32p, f32p, i64]),
         "fdmoe_debug_gemm": (i32, [i32, i32, f32p, f32p, f32p]),
     }
@@ -502,6 +503,18 @@ class Operator:
 
     def sync(self):
         _check(lib().fdmoe_sync(self._h))
+
+    def trace(self, local_rank: int = 0) -> np.ndarray:
+        """Per-CTA phase timestamps of the last launch (ns, relative to the earliest CTA start):
+        columns start, gate, barrier, dispatch, ffn, combine, end, ffn_tiles."""
+        info = self.info()
+        buf = np.zeros((info["ctas_per_rank"], 8), np.uint64)
+        n = C.c_int32()
+        _check(lib().fdmoe_read_trace(self._h, local_rank, _ptr(buf), buf.size, C.byref(n)))
+        t = buf.astype(np.int64)
+        t0 = t[:, 0].min()
+        t[:, :7] -= t0
+        return t
 
     def last_kernel_ms(self) -> float:
         """Device time of the most recent layer launch (CUDA events around it, max over devices)."""

@@ -13,13 +13,14 @@ constexpr int kBM = 128;            // rows per FFN tile (TMEM lanes)
 constexpr int kBN = 256;            // columns per FFN tile (TMEM columns per accumulator)
 constexpr int kAccStages = 2;       // TMEM accumulators (2 x 256 = all 512 columns)
 constexpr int kTaskRing = 4;        // producer -> MMA/epilogue task ring
-constexpr int kGateTok = 32;        // tokens per gate block
+constexpr int kGateTok = 16;        // tokens per gate block (slot-assignment / combine granule)
 constexpr int kGateKC = 32;         // K chunk of the exact gate
 constexpr int kMaxExperts = 256;    // E_total envelope of the exact SIMT gate
 constexpr int kMaxRanks = 64;       // P envelope (peer table size)
 constexpr int kMaxSrcPerTile = 8;   // packet_rows >= 16 -> <= 8 packets per 128-row tile
-constexpr int kCombineTok = 32;     // tokens per combine task
+constexpr int kCombineTok = 16;     // tokens per combine task (== kGateTok)
 constexpr int kMaxLocalRanks = 8;   // ranks per launch (virtual ranks on one GPU)
+constexpr int kTracePts = 8;        // start, gate, barrier, dispatch, gemm, combine, end, tiles
 
 enum Prec : int { kFP32 = 0, kBF16 = 1 };
 
@@ -65,6 +66,7 @@ struct alignas(64) RankCtx {
     uint32_t* g0done;          // [E_local][MT] GEMM0 tiles completed per row tile
     uint32_t* err;             // [4] error word: code, where, a, b
     unsigned long long* stats; // [8] gemm0, gemm1, combine tasks, dispatch rows, ...
+    unsigned long long* trace; // [ctas][kTracePts] %globaltimer per phase boundary (device trace)
     int32_t rank;
 };
 

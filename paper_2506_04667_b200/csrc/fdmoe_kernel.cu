@@ -181,88 +181,154 @@ __device__ bool rank_barrier(const LaunchParams& P, const RankCtx& R, unsigned l
 }
 
 // ================================================================ phase 1: exact gate
-// Smem: sL[kGateTok][Ep] logits/probs, sA[kGateKC][kGateTok] (A chunk, transposed),
-//       sW[kGateKC][Ep] (Wg chunk), sCnt[Ep] CTA-level pick counts.
+// Each CTA owns a contiguous, balanced token range (its gate blocks [b0, b1)), processed in
+// sub-tiles of <= 64 tokens. Logits are FP32 sequential dot products over x ascending with a
+// separately rounded multiply and add (gate.hpp:77-81 as compiled with -ffp-contract=off);
+// each thread owns 4 tokens x 8 experts and streams K through a 3-stage cp.async ring:
+//   sA[stage][64][36]  token rows (32 K values + 4 pad floats: conflict-free column reads)
+//   sW[stage][32][Ep]  Wg rows
+// then one warp per token does max / glibc-exp / sequential sum / divide / top-k.
+constexpr int kGateSub = 64;
+constexpr int kGateStages = 3;
+constexpr int kGateApitch = kGateKC + 4;
+constexpr int kGateSmemBytes = (kGateSub * kMaxExperts + kGateStages * kGateSub * kGateApitch +
+                                kGateStages * kGateKC * kMaxExperts + kMaxExperts) * 4;
+static_assert(kGateTok <= 32, "slot assignment maps one gate block onto one warp");
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+                 "r"(valid ? 16 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ void gate_token_range(const LaunchParams& P, int cta, int& tokA, int& tokB, int& b0,
+                                                 int& b1) {
+    const int nblk = (P.S + kGateTok - 1) / kGateTok;
+    b0 = (int)((long long)nblk * cta / P.ctas_per_rank);
+    b1 = (int)((long long)nblk * (cta + 1) / P.ctas_per_rank);
+    tokA = b0 * kGateTok;
+    tokB = min(P.S, b1 * kGateTok);
+}
+
 __device__ void gate_phase(const LaunchParams& P, const RankCtx& R, const float* __restrict__ A, int cta,
                            uint8_t* smem) {
-    const int E = P.E, H = P.H, S = P.S, K = P.k;
+    const int E = P.E, H = P.H, K = P.k;
     const int Ep = (E + 7) & ~7;
-    float* sL = reinterpret_cast<float*>(smem);
-    float* sA = sL + kGateTok * Ep;
-    float* sW = sA + kGateKC * kGateTok;
-    int* sCnt = reinterpret_cast<int*>(sW + kGateKC * Ep);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    float* sL = reinterpret_cast<float*>(smem);                                   // [64][Ep]
+    float* sA = sL + kGateSub * Ep;                                              // [stages][64][36]
+    float* sW = sA + kGateStages * kGateSub * kGateApitch;                       // [stages][32][Ep]
+    int* sCnt = reinterpret_cast<int*>(sW + kGateStages * kGateKC * Ep);        // [Ep]
     for (int e = tid; e < Ep; e += kThreads) sCnt[e] = 0;
+    const bool w_vec = (E & 3) == 0;
 
-    const int nblk = (S + kGateTok - 1) / kGateTok;
-    const int b0 = (int)((long long)nblk * cta / P.ctas_per_rank);
-    const int b1 = (int)((long long)nblk * (cta + 1) / P.ctas_per_rank);
-    const int n_eg = Ep / 8;                 // expert groups of 8
-    const int n_items = (kGateTok / 2) * n_eg;  // token pairs x expert groups (<= 512)
+    int tokA, tokB, b0, b1;
+    gate_token_range(P, cta, tokA, tokB, b0, b1);
+    const int ntok = tokB - tokA;
+    const int nsub = (ntok + kGateSub - 1) / kGateSub;
+    const int n_eg = Ep / 8;
+    const int nk = H / kGateKC;   // envelope: H % 32 == 0
 
-    for (int blk = b0; blk < b1; ++blk) {
-        const int tok0 = blk * kGateTok;
-        float acc[2][2][8];
+    for (int si = 0; si < nsub; ++si) {
+        // balanced sub-tiles, multiples of 4 tokens
+        const int s0 = (int)((long long)ntok * si / nsub) & ~3;
+        const int s1 = si + 1 == nsub ? ntok : ((int)((long long)ntok * (si + 1) / nsub) & ~3);
+        const int ts = s1 - s0;
+        const int n_tg = (ts + 3) / 4;
+        const int n_items = n_tg * n_eg;
+        const float* Abase = A + (size_t)(tokA + s0) * H;
+
+        auto load_stage = [&](int st, int kb) {
+            float* a = sA + st * kGateSub * kGateApitch;
+            float* w = sW + st * kGateKC * Ep;
+            const int k0 = kb * kGateKC;
+            for (int i = tid; i < kGateSub * 8; i += kThreads) {
+                const int t = i >> 3, c = i & 7;
+                const bool ok = t < ts;
+                cp_async16(a + t * kGateApitch + c * 4, Abase + (size_t)(ok ? t : 0) * H + k0 + c * 4, ok);
+            }
+            if (w_vec) {
+                const int cpr = Ep / 4;
+                for (int i = tid; i < kGateKC * cpr; i += kThreads) {
+                    const int kk = i / cpr, c = i % cpr;
+                    const bool ok = c * 4 < E;
+                    cp_async16(w + kk * Ep + c * 4, R.wg + (size_t)(k0 + kk) * E + (ok ? c * 4 : 0), ok);
+                }
+            } else {
+                for (int i = tid; i < kGateKC * Ep; i += kThreads) {
+                    const int kk = i / Ep, e = i % Ep;
+                    w[kk * Ep + e] = e < E ? R.wg[(size_t)(k0 + kk) * E + e] : 0.0f;
+                }
+            }
+            cp_async_commit();
+        };
+
+        float acc[2][4][8];
 #pragma unroll
         for (int it = 0; it < 2; ++it)
 #pragma unroll
-            for (int i = 0; i < 2; ++i)
+            for (int i = 0; i < 4; ++i)
 #pragma unroll
                 for (int j = 0; j < 8; ++j) acc[it][i][j] = 0.0f;
 
-        for (int k0 = 0; k0 < H; k0 += kGateKC) {
-            const int kc = min(kGateKC, H - k0);
+        __syncthreads();   // previous sub-tile's readers of sA/sW/sL are done
+        for (int st = 0; st < kGateStages - 1; ++st)
+            if (st < nk) load_stage(st, st); else cp_async_commit();
+        for (int kb = 0; kb < nk; ++kb) {
+            const int st = kb % kGateStages;
+            if (kb + kGateStages - 1 < nk) load_stage((kb + kGateStages - 1) % kGateStages, kb + kGateStages - 1);
+            else cp_async_commit();
+            cp_async_wait<kGateStages - 1>();
             __syncthreads();
-            for (int i = tid; i < kGateTok * kGateKC; i += kThreads) {
-                const int t = i / kGateKC, kk = i % kGateKC;
-                const int tok = tok0 + t;
-                sA[kk * kGateTok + t] = (tok < S && kk < kc) ? A[(size_t)tok * H + k0 + kk] : 0.0f;
-            }
-            for (int i = tid; i < kGateKC * Ep; i += kThreads) {
-                const int kk = i / Ep, e = i % Ep;
-                sW[kk * Ep + e] = (kk < kc && e < E) ? R.wg[(size_t)(k0 + kk) * E + e] : 0.0f;
-            }
-            __syncthreads();
+            const float* a = sA + st * kGateSub * kGateApitch;
+            const float* w = sW + st * kGateKC * Ep;
 #pragma unroll
             for (int it = 0; it < 2; ++it) {
                 const int item = tid + it * kThreads;
                 if (item < n_items) {
                     const int tg = item / n_eg, eg = item % n_eg;
-                    for (int kk = 0; kk < kc; ++kk) {
-                        const float2 a = *reinterpret_cast<const float2*>(&sA[kk * kGateTok + 2 * tg]);
-                        const float4 w0 = *reinterpret_cast<const float4*>(&sW[kk * Ep + 8 * eg]);
-                        const float4 w1 = *reinterpret_cast<const float4*>(&sW[kk * Ep + 8 * eg + 4]);
+                    const float* ar = a + (4 * tg) * kGateApitch;
+                    const float* wr = w + 8 * eg;
+#pragma unroll 8
+                    for (int kk = 0; kk < kGateKC; ++kk) {
+                        const float a0 = ar[kk], a1 = ar[kGateApitch + kk], a2 = ar[2 * kGateApitch + kk],
+                                    a3 = ar[3 * kGateApitch + kk];
+                        const float4 w0 = *reinterpret_cast<const float4*>(wr + kk * Ep);
+                        const float4 w1 = *reinterpret_cast<const float4*>(wr + kk * Ep + 4);
                         const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+                        const float av[4] = {a0, a1, a2, a3};
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            acc[it][0][j] = __fadd_rn(acc[it][0][j], __fmul_rn(a.x, wv[j]));
-                            acc[it][1][j] = __fadd_rn(acc[it][1][j], __fmul_rn(a.y, wv[j]));
-                        }
+                        for (int i = 0; i < 4; ++i)
+#pragma unroll
+                            for (int j = 0; j < 8; ++j)
+                                acc[it][i][j] = __fadd_rn(acc[it][i][j], __fmul_rn(av[i], wv[j]));
                     }
                 }
             }
+            __syncthreads();   // stage st may be refilled next iteration
         }
-        __syncthreads();
+        cp_async_wait<0>();
 #pragma unroll
         for (int it = 0; it < 2; ++it) {
             const int item = tid + it * kThreads;
             if (item < n_items) {
                 const int tg = item / n_eg, eg = item % n_eg;
 #pragma unroll
-                for (int i = 0; i < 2; ++i)
+                for (int i = 0; i < 4; ++i)
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) sL[(2 * tg + i) * Ep + 8 * eg + j] = acc[it][i][j];
+                    for (int j = 0; j < 8; ++j) sL[(4 * tg + i) * Ep + 8 * eg + j] = acc[it][i][j];
             }
         }
         __syncthreads();
 
-        // softmax + top-k: one warp per token (4 tokens per warp)
-        for (int t = warp; t < kGateTok; t += kThreads / 32) {
-            const int tok = tok0 + t;
-            if (tok >= S) continue;
+        // softmax + top-k: one warp per token
+        for (int t = warp; t < ts; t += kThreads / 32) {
+            const int tok = tokA + s0 + t;
             float* row = sL + t * Ep;
-            // max (exact and order-free; std::max semantics are irrelevant to the
-            // result because only x - max feeds expf and ties give identical values)
+            // max is exact and order-free (x - max only feeds expf; +-0 ties give equal results)
             float mx = row[0];
             for (int e = lane; e < E; e += 32) mx = fmaxf(mx, row[e]);
 #pragma unroll
@@ -279,12 +345,14 @@ __device__ void gate_phase(const LaunchParams& P, const RankCtx& R, const float*
                 R.g_phi[(size_t)tok * E + e] = p;
             }
             __syncwarp();
-            // top-k by repeated argmax; ties -> lower expert index
-            uint32_t taken = 0;   // bit j: expert lane + 32*j taken
+            // top-k by repeated argmax on p; ties -> lower expert index (gate.hpp:41-51)
+            uint32_t taken = 0;   // bit jj: expert lane + 32*jj taken
             float denom = 0.0f;
-            int pe[8];
             float pv[8];
-            for (int j = 0; j < K; ++j) {
+            int pe[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (j >= K) break;
                 float bv = -1.0f;
                 int bi = 0x7fffffff;
                 for (int e = lane, jj = 0; e < E; e += 32, ++jj) {
@@ -299,22 +367,20 @@ __device__ void gate_phase(const LaunchParams& P, const RankCtx& R, const float*
                     if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
                 }
                 if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
-                if (j < 8) { pe[j] = bi; pv[j] = bv; }
+                pe[j] = bi;
+                pv[j] = bv;
                 denom = __fadd_rn(denom, bv);   // pick order (gate.hpp:92)
-                if (lane == 0) {
-                    R.pick_e[(size_t)tok * K + j] = bi;
-                    atomicAdd(&sCnt[bi], 1);
-                }
             }
             if (lane == 0) {
-                for (int j = 0; j < K; ++j) {
-                    const float p = j < 8 ? pv[j] : row[R.pick_e[(size_t)tok * K + j]];
-                    R.pick_w[(size_t)tok * K + j] = denom > 0.0f ? __fdiv_rn(p, denom) : 0.0f;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    if (j >= K) break;
+                    R.pick_e[(size_t)tok * K + j] = pe[j];
+                    R.pick_w[(size_t)tok * K + j] = denom > 0.0f ? __fdiv_rn(pv[j], denom) : 0.0f;
+                    atomicAdd(&sCnt[pe[j]], 1);
                 }
             }
-            (void)pe;
         }
-        __syncthreads();
     }
     __syncthreads();
     for (int e = tid; e < E; e += kThreads) R.cnt_cta[(size_t)cta * E + e] = sCnt[e];
@@ -359,10 +425,8 @@ __device__ void dispatch_phase(const LaunchParams& P, const RankCtx& R, const fl
     }
     __syncthreads();
 
-    const int nblk = (S + kGateTok - 1) / kGateTok;
-    const int b0 = (int)((long long)nblk * cta / P.ctas_per_rank);
-    const int b1 = (int)((long long)nblk * (cta + 1) / P.ctas_per_rank);
-    const int tokA = b0 * kGateTok, tokB = min(S, b1 * kGateTok);
+    int tokA, tokB, b0, b1;
+    gate_token_range(P, cta, tokA, tokB, b0, b1);
 
     // slot assignment in ascending token order (one warp, lane = token in block):
     // slot = (picks of e by earlier CTAs) + (by earlier blocks of this CTA) + (by earlier
@@ -370,7 +434,7 @@ __device__ void dispatch_phase(const LaunchParams& P, const RankCtx& R, const fl
     if (warp == 0) {
         for (int blk = b0; blk < b1; ++blk) {
             const int tok = blk * kGateTok + lane;
-            const bool valid = tok < S;
+            const bool valid = lane < kGateTok && tok < S;
             int mye[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) mye[j] = (valid && j < K) ? R.pick_e[(size_t)tok * K + j] : -1;
@@ -489,6 +553,9 @@ struct GemmCfg {
     static constexpr int CTRL_BYTES = 1024;
     static constexpr int SMEM_BYTES = RING_BYTES + CTRL_BYTES;
 };
+
+static_assert(kGateSmemBytes <= GemmCfg<kFP32>::RING_BYTES && kGateSmemBytes <= GemmCfg<kBF16>::RING_BYTES,
+              "gate scratch must not overlap the GEMM control block");
 
 struct GemmCtrl {
     uint64_t full[4], empty[4];
@@ -794,8 +861,14 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
 
 // ================================================================ phase 4: combine
 static_assert(kCombineTok == kGateTok, "combine tasks are aligned with gate blocks (blk_ready)");
+// O[t] = sum over the token's kept picks, in pick order, of w * y (oracle.hpp:102-107): one warp
+// per token, 16-byte column chunks, all of a token's landed rows loaded before the adds.
+// The CTA first waits once for every combine tile this rank expects (n_e = kept rows per expert,
+// saved from the dispatch phase in sN), so the per-token loop has no flag traffic.
+constexpr int kCombUnroll = 4;
+
 __device__ void combine_phase(const LaunchParams& P, const RankCtx& R, float* __restrict__ O, uint8_t* smem,
-                              unsigned long long* stat) {
+                              const int* __restrict__ sN, unsigned long long* stat) {
     const int S = P.S, H = P.H, K = P.k;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t par = P.epoch & 1u;
@@ -804,50 +877,79 @@ __device__ void combine_phase(const LaunchParams& P, const RankCtx& R, float* __
     const float* yc = reinterpret_cast<const float*>(R.peer_heap[R.rank] + R.hl.yc);
     const unsigned long long* cflag =
         reinterpret_cast<const unsigned long long*>(R.peer_heap[R.rank] + R.hl.cflag[par]);
+
+    // (1) every expected combine tile has landed (acquire), then CTA barrier
+    const int nflags = P.E * P.RBF * P.NB1;
+    bool ok = true;
+    for (int f = tid; f < nflags && ok; f += kThreads) {
+        const int e = f / (P.RBF * P.NB1);
+        const int rbf = (f / P.NB1) % P.RBF;
+        if (sN[e] > rbf * kBM)
+            if (wait_epoch_flag(P, R, cflag + f, 400) < 0) ok = false;
+    }
+    if (!__syncthreads_and(ok)) return;
+
+    const int H4 = H >> 2;
     while (true) {
         __syncthreads();
-        if (tid == 0) sTask[0] = ld_volatile_u32(P.abort_flag) ? ntask : (int)atomicAdd(R.comb_head, 1u);
+        if (tid == 0) {
+            int t = ld_volatile_u32(P.abort_flag) ? ntask : (int)atomicAdd(R.comb_head, 1u);
+            // routing of these tokens was written by the CTA that gated them (dispatch phase)
+            if (t < ntask && !wait_counter_eq(P, R, R.blk_ready + t, P.epoch, 401)) t = ntask;
+            sTask[0] = t;
+        }
         __syncthreads();
         const int t = sTask[0];
         if (t >= ntask) break;
-        if (tid == 0) {
-            stat[2]++;
-            // routing of these tokens was written by the CTA that gated them (dispatch phase)
-            if (!wait_counter_eq(P, R, R.blk_ready + t, P.epoch, 401)) sTask[1] = 1;
-            else sTask[1] = 0;
-        }
-        __syncthreads();
-        if (sTask[1]) break;
+        if (tid == 0) stat[2]++;
         for (int i = warp; i < kCombineTok; i += kThreads / 32) {
             const int tok = t * kCombineTok + i;
             if (tok >= S) break;
-            // wait for every combine tile this token needs (lanes poll column blocks)
-            bool ok = true;
-            for (int j = 0; j < K && ok; ++j) {
-                const int slot = R.pick_slot[(size_t)tok * K + j];
-                if (slot < 0) continue;
-                const int e = R.pick_e[(size_t)tok * K + j];
-                const int rbf = P.Cp >= kBM ? slot / kBM : 0;
-                for (int nb = lane; nb < P.NB1; nb += 32)
-                    if (wait_epoch_flag(P, R, cflag + ((size_t)e * P.RBF + rbf) * P.NB1 + nb, 400) < 0) ok = false;
+            // this token's picks, one per lane, then broadcast
+            int my_e = 0, my_s = -1;
+            float my_w = 0.0f;
+            if (lane < K) {
+                my_s = R.pick_slot[(size_t)tok * K + lane];
+                my_e = R.pick_e[(size_t)tok * K + lane];
+                my_w = R.pick_w[(size_t)tok * K + lane];
             }
-            if (!__all_sync(0xffffffffu, ok)) break;   // aborted: the next task fetch sees the abort word
-            __syncwarp();   // other lanes' acquires order this lane's reads of the landed rows
+            const float4* yrow[8];
+            float wj[8];
+            int nk = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (j >= K) break;
+                const int sj = __shfl_sync(0xffffffffu, my_s, j);
+                const int ej = __shfl_sync(0xffffffffu, my_e, j);
+                const float w = __shfl_sync(0xffffffffu, my_w, j);
+                yrow[j] = reinterpret_cast<const float4*>(yc + ((size_t)ej * P.C + (sj < 0 ? 0 : sj)) * H);
+                wj[j] = sj < 0 ? 0.0f : w;
+                nk += sj < 0 ? 0 : (1 << j);   // bitmask of kept picks
+            }
             float4* orow = reinterpret_cast<float4*>(O + (size_t)tok * H);
-            for (int c = lane; c < (H >> 2); c += 32) {
-                float4 acc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-                for (int j = 0; j < K; ++j) {
-                    const int slot = R.pick_slot[(size_t)tok * K + j];
-                    if (slot < 0) continue;   // capacity-dropped: zero contribution
-                    const int e = R.pick_e[(size_t)tok * K + j];
-                    const float w = R.pick_w[(size_t)tok * K + j];
-                    const float4 y = *(reinterpret_cast<const float4*>(yc + ((size_t)e * P.C + slot) * H) + c);
-                    acc.x = __fadd_rn(acc.x, __fmul_rn(w, y.x));
-                    acc.y = __fadd_rn(acc.y, __fmul_rn(w, y.y));
-                    acc.z = __fadd_rn(acc.z, __fmul_rn(w, y.z));
-                    acc.w = __fadd_rn(acc.w, __fmul_rn(w, y.w));
+            for (int c0 = lane; c0 < H4; c0 += 32 * kCombUnroll) {
+                float4 acc[kCombUnroll];
+#pragma unroll
+                for (int u = 0; u < kCombUnroll; ++u) acc[u] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    if (j >= K) break;
+                    if (!(nk & (1 << j))) continue;   // capacity-dropped: zero contribution
+                    float4 y[kCombUnroll];
+#pragma unroll
+                    for (int u = 0; u < kCombUnroll; ++u)
+                        if (c0 + 32 * u < H4) y[u] = __ldcs(yrow[j] + c0 + 32 * u);
+#pragma unroll
+                    for (int u = 0; u < kCombUnroll; ++u) {
+                        acc[u].x = __fadd_rn(acc[u].x, __fmul_rn(wj[j], y[u].x));
+                        acc[u].y = __fadd_rn(acc[u].y, __fmul_rn(wj[j], y[u].y));
+                        acc[u].z = __fadd_rn(acc[u].z, __fmul_rn(wj[j], y[u].z));
+                        acc[u].w = __fadd_rn(acc[u].w, __fmul_rn(wj[j], y[u].w));
+                    }
                 }
-                orow[c] = acc;
+#pragma unroll
+                for (int u = 0; u < kCombUnroll; ++u)
+                    if (c0 + 32 * u < H4) __stcs(orow + c0 + 32 * u, acc[u]);
             }
         }
     }
@@ -857,7 +959,9 @@ __device__ void combine_phase(const LaunchParams& P, const RankCtx& R, float* __
 template <int PREC>
 __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_constant__ LaunchParams P) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // align to 1024 B (SWIZZLE_128B atoms) by offsetting the shared array itself, so nvcc keeps
+    // the shared address space (LDS/STS, not generic LD/ST) for every pointer derived from it
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     using Cfg = GemmCfg<PREC>;
     const int rl = blockIdx.x / P.ctas_per_rank;
     const int cta = blockIdx.x % P.ctas_per_rank;
@@ -866,7 +970,10 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
     float* O = P.out[rl];
     const int tid = threadIdx.x, warp = tid >> 5;
     __shared__ unsigned long long s_stat[4];
+    __shared__ int s_n_expert[kMaxExperts];   // kept rows per expert of this rank (dispatch -> combine)
     if (tid < 4) s_stat[tid] = 0;
+    unsigned long long* trace = R.trace + (size_t)cta * kTracePts;
+    if (tid == 0) trace[0] = globaltimer();
 
     GemmCtrl& G = *reinterpret_cast<GemmCtrl*>(smem + Cfg::RING_BYTES);
     uint8_t* ring = smem;
@@ -889,11 +996,15 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
 
     // phase 1: exact gate (uses the smem ring as scratch)
     gate_phase(P, R, A, cta, smem);
+    if (tid == 0) trace[1] = globaltimer();
     if (!rank_barrier(P, R, P.launch_seq)) goto done;
+    if (tid == 0) trace[2] = globaltimer();
 
     // phase 2: slot assignment + dispatch
     dispatch_phase(P, R, A, cta, smem);
     __syncthreads();
+    for (int e = tid; e < P.E; e += kThreads) s_n_expert[e] = reinterpret_cast<const int*>(smem)[kMaxExperts + e];
+    if (tid == 0) trace[3] = globaltimer();
 
     // phase 3: expert FFN tiles
     if (tid == 0) {
@@ -913,12 +1024,18 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
         gemm_epilogue<PREC>(P, R, G, s_stat);
     }
     __syncthreads();
+    if (tid == 0) trace[4] = globaltimer();
 
     // phase 4: combine
-    if (ld_volatile_u32(P.abort_flag) == 0) combine_phase(P, R, O, smem, s_stat);
+    if (ld_volatile_u32(P.abort_flag) == 0) combine_phase(P, R, O, smem, s_n_expert, s_stat);
+    if (tid == 0) trace[5] = globaltimer();
 
 done:
     __syncthreads();
+    if (tid == 0) {
+        trace[6] = globaltimer();
+        trace[7] = s_stat[0] + s_stat[1];
+    }
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc(tmem_base, 512);
@@ -975,7 +1092,7 @@ __global__ void __launch_bounds__(kThreads, 1) debug_gemm_kernel(const __grid_co
                                                                  const __grid_constant__ CUtensorMap tb1, int K,
                                                                  float* D, uint32_t* abort_flag) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     using Cfg = GemmCfg<PREC>;
     GemmCtrl& G = *reinterpret_cast<GemmCtrl*>(smem + Cfg::RING_BYTES);
     const int tid = threadIdx.x, warp = tid >> 5;

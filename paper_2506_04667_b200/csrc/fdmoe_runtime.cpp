@@ -111,6 +111,8 @@ struct RankRes {
     float* tbl_w = nullptr;
     int32_t* slot_counts = nullptr;
     uint32_t* blk_ready = nullptr;
+    unsigned long long* trace = nullptr;
+    int ctas = 0;
     uint8_t* ctrl = nullptr;        // bar | heads | err | stats | sent | g0done
     float* in_buf = nullptr;
     float* out_buf = nullptr;
@@ -193,6 +195,7 @@ fdmoe_status alloc_rank(fdmoe_handle* h, RankRes& r, int ctas_per_rank) {
     parts.push_back({(void**)&r.tbl_tok, (size_t)d.E * d.C * 4});
     parts.push_back({(void**)&r.tbl_w, (size_t)d.E * d.C * 4});
     parts.push_back({(void**)&r.slot_counts, (size_t)d.E * 4});
+    parts.push_back({(void**)&r.trace, (size_t)ctas_per_rank * kTracePts * 8});
     parts.push_back({(void**)&r.blk_ready, (size_t)(d.S + kGateTok - 1) / kGateTok * 4});
     parts.push_back({(void**)&r.ctrl, ctrl_bytes(d)});
     parts.push_back({(void**)&r.in_buf, (size_t)d.S * d.H * 4});
@@ -203,6 +206,8 @@ fdmoe_status alloc_rank(fdmoe_handle* h, RankRes& r, int ctas_per_rank) {
     r.scratch_bytes = total;
     size_t o = 0;
     for (auto& p : parts) { *p.first = r.scratch + o; o += align_up(p.second); }
+    r.ctas = ctas_per_rank;
+    CK(cudaMemset(r.trace, 0, (size_t)ctas_per_rank * kTracePts * 8));
     CK(cudaMemset(r.ctrl, 0, ctrl_bytes(d)));
     CK(cudaMemset(r.blk_ready, 0, (size_t)(d.S + kGateTok - 1) / kGateTok * 4));
     for (int pl = 0; pl < d.planes; ++pl) {   // padding rows of the weight planes stay finite
@@ -240,6 +245,7 @@ fdmoe_status build_ctx(fdmoe_handle* h) {
             c.g_phi = r.g_phi; c.pick_e = r.pick_e; c.pick_slot = r.pick_slot; c.pick_w = r.pick_w;
             c.cnt_cta = r.cnt_cta; c.tbl_tok = r.tbl_tok; c.tbl_w = r.tbl_w; c.slot_counts = r.slot_counts;
             c.blk_ready = r.blk_ready;
+            c.trace = r.trace;
             c.bar = reinterpret_cast<unsigned long long*>(r.ctrl + kCtrlBar);
             c.gemm_head = reinterpret_cast<uint32_t*>(r.ctrl + kCtrlGemm);
             c.comb_head = reinterpret_cast<uint32_t*>(r.ctrl + kCtrlComb);
@@ -258,7 +264,8 @@ fdmoe_status build_ctx(fdmoe_handle* h) {
 fdmoe_status check_errors(fdmoe_handle* h) {
     for (auto& g : h->groups) {
         CK(cudaSetDevice(g.dev));
-        CK(cudaStreamSynchronize(g.stream));
+        CK(cudaEventSynchronize(g.ev1));          // end of the launch, on whatever stream it ran
+        CK(cudaStreamSynchronize(g.stream));      // host-path copies queued behind it
     }
     fdmoe_status worst = FDMOE_OK;
     std::string msg;
@@ -616,6 +623,17 @@ fdmoe_status fdmoe_get_info(fdmoe_handle* h, fdmoe_info* info) {
     info->smem_bytes = h->groups[0].smem;
     info->num_sms = h->groups[0].num_sms;
     info->ranks_per_launch = (int32_t)h->groups[0].members.size();
+    return FDMOE_OK;
+}
+
+fdmoe_status fdmoe_read_trace(fdmoe_handle* h, int32_t local_rank, uint64_t* out, int32_t cap, int32_t* n_ctas) {
+    if (!h || local_rank < 0 || local_rank >= h->n_local) return fail(FDMOE_ERR_CONFIG, "bad rank");
+    RankRes& r = h->ranks[local_rank];
+    CK(cudaSetDevice(r.dev));
+    for (auto& g : h->groups) if (g.dev == r.dev) CK(cudaEventSynchronize(g.ev1));
+    const int n = std::min(cap / kTracePts, r.ctas);
+    CK(cudaMemcpy(out, r.trace, (size_t)n * kTracePts * 8, cudaMemcpyDeviceToHost));
+    if (n_ctas) *n_ctas = r.ctas;
     return FDMOE_OK;
 }
 

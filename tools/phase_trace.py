@@ -1,0 +1,20 @@
+"""Phase breakdown of one layer launch from the device trace (per-CTA %globaltimer stamps)."""
+import sys, json, numpy as np
+sys.path.insert(0, '.')
+import torch
+import paper_2506_04667_b200 as fd
+S, E = int(sys.argv[1]) if len(sys.argv) > 1 else 16384, int(sys.argv[2]) if len(sys.argv) > 2 else 128
+prec = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+cfg = fd.MoeConfig(tokens_per_device=S, embed_dim=2048, ffn_dim=2048, experts_total=E, devices=1, topk=2,
+                   tile_rows=128, tile_cols=64, precision=prec)
+op = fd.Operator(cfg); op.set_weights(fd.make_model(cfg))
+x = torch.from_numpy(fd.make_shards(cfg)[0]).cuda(); y = torch.empty_like(x)
+st = torch.cuda.Stream(); torch.cuda.set_stream(st)
+for _ in range(4):
+    op.forward_device([x.data_ptr()], [y.data_ptr()], [st.cuda_stream]); op.sync()
+t = op.trace(0) / 1e3   # us
+names = ["start", "gate", "barrier", "dispatch", "ffn", "combine", "end"]
+print("kernel ms", op.last_kernel_ms())
+for i, n in enumerate(names):
+    print(f"{n:9s} min {t[:, i].min():9.1f}  med {np.median(t[:, i]):9.1f}  max {t[:, i].max():9.1f} us")
+print("ffn tiles per CTA: min", int(t[:, 7].min()), "max", int(t[:, 7].max()), "sum", int(t[:, 7].sum()))
