@@ -196,9 +196,10 @@ fdmoe_status fdmoe_read_trace(fdmoe_handle* h, int32_t local_rank, uint64_t* out
 /* ---- diagnostics (tests only; not part of the reference surface) -------------------- */
 /* The kernel's glibc-expf restatement on n host floats (runs on device 0). */
 fdmoe_status fdmoe_debug_expf(const float* x, float* y, int64_t n);
-/* One 128x256 tile through the layer's TMA -> tcgen05.mma -> TMEM path:
- * D[128 x 256] = A[128 x K] * B[256 x K]^T, host row-major FP32 (K % 64 == 0). */
-fdmoe_status fdmoe_debug_gemm(int32_t precision, int32_t K, const float* A, const float* B, float* D);
+/* One 128x128 tile through the layer's FFN machinery (weight rows -> registers -> TMEM operand,
+ * token rows via TMA -> smem operand, tcgen05.mma, TMEM epilogue):
+ * D[f][t] = sum_k W[f][k] * X[t][k]; W, X: 128 x K host row-major FP32 (K % 64 == 0). */
+fdmoe_status fdmoe_debug_gemm(int32_t precision, int32_t K, const float* W, const float* X, float* D);
 
 #ifdef __cplusplus
 }

@@ -8,10 +8,16 @@
 namespace fdmoe {
 
 // ---------------------------------------------------------------- constants
-constexpr int kThreads = 256;       // 8 warps: w0 TMA, w1 MMA, w2 TMEM alloc, w4-7 epilogue
-constexpr int kBM = 128;            // rows per FFN tile (TMEM lanes)
-constexpr int kBN = 256;            // columns per FFN tile (TMEM columns per accumulator)
-constexpr int kAccStages = 2;       // TMEM accumulators (2 x 256 = all 512 columns)
+// 12 warps: w0 tile scheduler + TMA (token operand), w1 tcgen05.mma issuer, w2 TMEM allocator,
+// w3 spare, w4-7 weight loaders (global -> registers -> tf32 hi/lo split -> TMEM),
+// w8-11 epilogue (TMEM -> registers -> bias/activation -> global / peer stores)
+constexpr int kThreads = 384;
+constexpr int kBM = 128;            // tokens per row tile of an expert's receive region
+constexpr int kBF = 128;            // output features per FFN tile (MMA M = TMEM lanes)
+constexpr int kNT = 128;            // tokens per FFN tile (MMA N = accumulator columns)
+constexpr int kAccStages = 2;       // TMEM accumulators: 2 x 128 columns
+constexpr int kAStages = 4;         // TMEM weight-operand stages (columns 256..511)
+constexpr int kBN = kBF;            // feature block width used by the flag / task arithmetic
 constexpr int kTaskRing = 4;        // producer -> MMA/epilogue task ring
 constexpr int kGateTok = 16;        // tokens per gate block (slot-assignment / combine granule)
 constexpr int kGateKC = 32;         // K chunk of the exact gate
@@ -38,8 +44,8 @@ struct HeapLayout {
 struct alignas(64) RankCtx {
     CUtensorMap tm_x[2][2];    // [parity][hi|lo]  rows = E_local*RP, cols = H
     CUtensorMap tm_c1[2];      // [hi|lo]          rows = E_local*RP, cols = D
-    CUtensorMap tm_w1[2];      // [hi|lo]          rows = E_local*D,  cols = H (W1^T, K-major)
-    CUtensorMap tm_w2[2];      // [hi|lo]          rows = E_local*H,  cols = D (W2^T, K-major)
+    CUtensorMap tm_w1;         // W1^T [E_local*D (+pad)][H], FP32 (split on chip) or bf16, box 128 rows
+    CUtensorMap tm_w2;         // W2^T [E_local*H (+pad)][D]
 
     uint8_t* peer_heap[kMaxRanks];   // heap base of rank q as mapped here (q == rank: own)
     HeapLayout hl;
@@ -222,6 +228,44 @@ __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64
         ::"r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// A operand from TMEM (the expert's weight tile), B from shared memory (tokens).
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}"
+        ::"r"(d_tmem), "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
+        ::"r"(d_tmem), "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// 32 lanes x 16 consecutive 32-bit columns from registers (thread t -> its lane's row).
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+        ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+          "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ float4 ld_stream_f4(const void* p) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                      smem_u32(bar))

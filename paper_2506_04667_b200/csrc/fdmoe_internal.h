@@ -16,8 +16,7 @@ fdmoe_status fail(fdmoe_status s, const std::string& msg);
 int layer_smem_bytes(int prec);
 int layer_max_blocks_per_sm(int prec, int smem);
 cudaError_t launch_layer(const LaunchParams& p, int grid, int smem, cudaStream_t stream);
-cudaError_t launch_prep_transpose(const float* W, int El, int Rr, int Cc, void* hi, void* lo, int prec,
-                                  cudaStream_t s);
+cudaError_t launch_prep_transpose(const float* W, int El, int Rr, int Cc, void* out, int prec, cudaStream_t s);
 cudaError_t launch_debug_expf(const float* x, float* y, long long n, cudaStream_t s);
 cudaError_t launch_debug_gemm(int prec, const CUtensorMap* t, int K, float* D, uint32_t* abort_flag,
                               cudaStream_t s);

@@ -463,8 +463,11 @@ __device__ void dispatch_phase(const LaunchParams& P, const RankCtx& R, const fl
                 }
             }
             __syncwarp();
-            if (valid)
-                for (int j = 0; j < K; ++j) atomicAdd(&sRun[mye[j]], 1);
+            if (valid) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (j < K) atomicAdd(&sRun[mye[j]], 1);
+            }
             __syncwarp();
             // this block's picks/slots/weights are final: the combine (any CTA) acquires this
             __threadfence();
@@ -511,11 +514,14 @@ __device__ void dispatch_phase(const LaunchParams& P, const RankCtx& R, const fl
         }
     }
     __syncthreads();
-    // last CTA to complete a packet publishes its signal (pgas.hpp:99-113 semantics)
+    // one system-scope fence orders every row this CTA pushed (cumulative through bar.sync)
+    // before the packet counters below; the last CTA to complete a packet publishes its signal
+    // with release semantics (pgas.hpp:99-113)
+    if (tid == 0) __threadfence_system();
+    __syncthreads();
     for (int e = tid; e < E; e += kThreads) {
         const int kept = sKept[e];
         if (kept <= 0) continue;
-        __threadfence_system();
         const uint32_t old = atomicAdd(&R.sent[e], (uint32_t)kept);
         if ((int)(old + kept) == sN[e]) {
             __threadfence_system();
@@ -530,59 +536,70 @@ __device__ void dispatch_phase(const LaunchParams& P, const RankCtx& R, const fl
 }
 
 // ================================================================ phase 3: expert FFN
+// Tile = (local expert le, feature block nb of 128 outputs, row tile m of 128 received tokens):
+//   D[f][t] = sum_k W^T[f][k] * X[t][k]     (GEMM0: K = H, W = W1;  GEMM1: K = D, W = W2, X = C1)
+// A operand (weights) lives in TMEM: loader warps read FP32 rows with coalesced 16-byte loads,
+// split them into tf32 hi/lo in registers and tcgen05.st both parts into a 4-stage TMEM ring —
+// weights cross HBM once at 4 bytes/element. B operand (tokens, already hi/lo-split at dispatch)
+// is TMA-staged in a SWIZZLE_128B smem ring. 3xTF32: lo*hi + hi*lo + hi*hi per k-step, FP32
+// accumulation in double-buffered TMEM accumulators. (runtime.hpp:652-699, tiled_blas.hpp:80-96)
 struct Task {
     int type;   // 0 = GEMM0, 1 = GEMM1, -1 = end
     int le, nb, m;
     int nsrc, src0;
     int cnt[kMaxSrcPerTile];   // valid rows per packet in the tile
-    int rows_lo[kMaxSrcPerTile];   // first tile row of each packet
 };
 
 template <int PREC>
 struct GemmCfg {
-    static constexpr int BK = PREC == kFP32 ? 32 : 64;          // 128-byte K rows (SWIZZLE_128B)
+    static constexpr int BK = PREC == kFP32 ? 32 : 64;          // K per stage: 128-byte rows (SWIZZLE_128B)
     static constexpr int ESZ = PREC == kFP32 ? 4 : 2;
-    static constexpr int A_BYTES = kBM * BK * ESZ;             // one A operand plane
-    static constexpr int B_BYTES = kBN * BK * ESZ;             // one B operand plane
-    static constexpr int PLANES = PREC == kFP32 ? 2 : 1;       // hi/lo split
-    static constexpr int STAGE_BYTES = (A_BYTES + B_BYTES) * PLANES;
-    static constexpr int STAGES = PREC == kFP32 ? 2 : 4;
+    static constexpr int B_BYTES = kNT * BK * ESZ;             // one token-operand plane per stage
+    static constexpr int PLANES = PREC == kFP32 ? 2 : 1;       // hi/lo split of the token operand
+    static constexpr int STAGE_BYTES = B_BYTES * PLANES;
+    static constexpr int STAGES = 4;                            // token ring
+    static constexpr int W_BYTES = kBF * BK * ESZ;             // weight tile per stage (raw FP32 / bf16)
+    static constexpr int WSTAGES = PREC == kFP32 ? 4 : 6;      // weight ring (TMA -> smem -> TMEM)
     static constexpr int KSTEP = PREC == kFP32 ? 8 : 16;       // K per tcgen05.mma
-    static constexpr uint32_t IDESC = umma_idesc(PREC == kFP32 ? 2u : 1u, kBM, kBN);
-    static constexpr int RING_BYTES = STAGE_BYTES * STAGES;
-    static constexpr int CTRL_BYTES = 1024;
-    static constexpr int SMEM_BYTES = RING_BYTES + CTRL_BYTES;
+    static constexpr int A_COLS = PREC == kFP32 ? 2 * BK : BK / 2;   // TMEM columns per weight stage
+    static constexpr uint32_t IDESC = umma_idesc(PREC == kFP32 ? 2u : 1u, kBF, kNT);
+    static constexpr int W_OFF = STAGE_BYTES * STAGES;
+    static constexpr int RING_BYTES = W_OFF + W_BYTES * WSTAGES;
+    static constexpr uint32_t TMEM_A0 = kAccStages * kNT;      // first weight-stage column
+    static_assert(TMEM_A0 + kAStages * A_COLS <= 512, "TMEM budget");
 };
 
-static_assert(kGateSmemBytes <= GemmCfg<kFP32>::RING_BYTES && kGateSmemBytes <= GemmCfg<kBF16>::RING_BYTES,
-              "gate scratch must not overlap the GEMM control block");
+// dynamic smem: [max(gate scratch, token ring)] [GemmCtrl]
+template <int PREC>
+struct SmemPlan {
+    static constexpr int REGION = ((kGateSmemBytes > GemmCfg<PREC>::RING_BYTES ? kGateSmemBytes
+                                                                                : GemmCfg<PREC>::RING_BYTES) +
+                                   1023) / 1024 * 1024;
+    static constexpr int TOTAL = REGION + 1024 /* ctrl */ + 1024 /* alignment slack */;
+};
 
 struct GemmCtrl {
-    uint64_t full[4], empty[4];
-    uint64_t tfull[kAccStages], tempty[kAccStages];
-    uint64_t qfull[kTaskRing], qempty[kTaskRing];
+    uint64_t full[8], empty[8];                      // token-operand smem ring
+    uint64_t wfull[8], wempty[8];                    // weight smem ring
+    uint64_t afull[kAStages], aempty[kAStages];      // weight-operand TMEM ring
+    uint64_t tfull[kAccStages], tempty[kAccStages];  // accumulators
+    uint64_t qfull[kTaskRing], qempty[kTaskRing];    // task ring
     uint32_t tmem_base;
     uint32_t pad;
     Task ring[kTaskRing];
 };
+constexpr int kTaskConsumers = 1 + 4 + 1;   // MMA warp, 4 loader warps, epilogue
 
 __device__ __forceinline__ void decode_task(const LaunchParams& P, uint32_t t, uint32_t n_g0, Task& tk) {
-    if (t < n_g0) {
-        tk.type = 0;
-        const uint32_t per_e = (uint32_t)P.NB0 * P.MT;
-        tk.le = t / per_e;
-        const uint32_t r = t % per_e;
-        tk.nb = r / P.MT;
-        tk.m = r % P.MT;
-    } else {
-        t -= n_g0;
-        tk.type = 1;
-        const uint32_t per_e = (uint32_t)P.NB1 * P.MT;
-        tk.le = t / per_e;
-        const uint32_t r = t % per_e;
-        tk.nb = r / P.MT;
-        tk.m = r % P.MT;
-    }
+    const bool g1 = t >= n_g0;
+    if (g1) t -= n_g0;
+    const uint32_t nbk = g1 ? (uint32_t)P.NB1 : (uint32_t)P.NB0;
+    const uint32_t per_e = nbk * P.MT;
+    tk.type = g1 ? 1 : 0;
+    tk.le = t / per_e;
+    const uint32_t r = t % per_e;
+    tk.nb = r / P.MT;   // consecutive tasks share the weight tile (e, nb) across row tiles m
+    tk.m = r % P.MT;
 }
 
 // Packets intersecting row tile m of an expert's receive region, and their signalled rows.
@@ -601,7 +618,6 @@ __device__ int resolve_tile_rows(const LaunchParams& P, const RankCtx& R, Task& 
         if (n < 0) return -1;
         const int v = max(0, min(kBM, (int)n - rb * kBM));
         tk.cnt[0] = v;
-        tk.rows_lo[0] = 0;
         total = v;
     } else {
         const int per = kBM / P.Cp;
@@ -613,29 +629,29 @@ __device__ int resolve_tile_rows(const LaunchParams& P, const RankCtx& R, Task& 
             const int64_t n = wait_epoch_flag(P, R, dflag + s, 301);
             if (n < 0) return -1;
             tk.cnt[s - s0] = (int)n;
-            tk.rows_lo[s - s0] = (s - s0) * P.Cp;
             total += (int)n;
         }
     }
     return total;
 }
 
+// warp 0, one lane: fetch tiles, resolve dependencies, stream the token operand
 template <int PREC>
 __device__ void gemm_producer(const LaunchParams& P, const RankCtx& R, uint8_t* ring, GemmCtrl& G) {
     using Cfg = GemmCfg<PREC>;
     const uint32_t n_g0 = (uint32_t)P.El * P.NB0 * P.MT;
     const uint32_t n_g1 = (uint32_t)P.El * P.NB1 * P.MT;
     const uint32_t par = P.epoch & 1u;
-    int stage = 0;
-    uint32_t phase = 0;
+    int stage = 0, wstage = 0;
+    uint32_t phase = 0, wphase = 0;
     int q = 0;
     uint32_t qphase = 0;
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < Cfg::PLANES; ++i) {
         tma_prefetch(&R.tm_x[par][i]);
         tma_prefetch(&R.tm_c1[i]);
-        tma_prefetch(&R.tm_w1[i]);
-        tma_prefetch(&R.tm_w2[i]);
     }
+    tma_prefetch(&R.tm_w1);
+    tma_prefetch(&R.tm_w2);
     while (true) {
         const uint32_t t = atomicAdd(R.gemm_head, 1u);
         Task tk;
@@ -644,7 +660,7 @@ __device__ void gemm_producer(const LaunchParams& P, const RankCtx& R, uint8_t* 
             decode_task(P, t, n_g0, tk);
             const int rows = resolve_tile_rows(P, R, tk);
             if (rows < 0) end = true;
-            else if (rows == 0) continue;   // empty tile: no GEMM0/GEMM1 work exists for it
+            else if (rows == 0) continue;   // empty row tile: no GEMM0/GEMM1 work exists for it
             else if (tk.type == 1) {
                 if (!wait_counter(P, R, R.g0done + (size_t)tk.le * P.MT + tk.m, (uint32_t)P.NB0, 302)) end = true;
             }
@@ -653,190 +669,255 @@ __device__ void gemm_producer(const LaunchParams& P, const RankCtx& R, uint8_t* 
         if (end) {
             G.ring[q].type = -1;
             mbar_arrive(&G.qfull[q]);
-            break;
+            return;
         }
         G.ring[q] = tk;
         mbar_arrive(&G.qfull[q]);
         if (++q == kTaskRing) { q = 0; qphase ^= 1u; }
 
-        // operands: generic-proxy writes (peer dispatch stores / local GEMM0 epilogue)
-        // were acquired above; order them before the async-proxy (TMA) reads.
+        // token rows were written by the generic proxy (peer dispatch stores / GEMM0 epilogues)
+        // and acquired above; order them before the async-proxy (TMA) reads
         fence_proxy_async_global();
-        const CUtensorMap* ta[2];
         const CUtensorMap* tb[2];
-        int ya, yb, nk;
-        if (tk.type == 0) {
-            ta[0] = &R.tm_x[par][0]; ta[1] = &R.tm_x[par][1];
-            tb[0] = &R.tm_w1[0]; tb[1] = &R.tm_w1[1];
-            ya = tk.le * P.RP + tk.m * kBM;
-            yb = tk.le * P.D + tk.nb * kBN;
-            nk = (P.H + Cfg::BK - 1) / Cfg::BK;
-        } else {
-            ta[0] = &R.tm_c1[0]; ta[1] = &R.tm_c1[1];
-            tb[0] = &R.tm_w2[0]; tb[1] = &R.tm_w2[1];
-            ya = tk.le * P.RP + tk.m * kBM;
-            yb = tk.le * P.H + tk.nb * kBN;
-            nk = (P.D + Cfg::BK - 1) / Cfg::BK;
-        }
+        const CUtensorMap* tw;
+        int yw;
+        if (tk.type == 0) { tb[0] = &R.tm_x[par][0]; tb[1] = &R.tm_x[par][1]; tw = &R.tm_w1; yw = tk.le * P.D; }
+        else { tb[0] = &R.tm_c1[0]; tb[1] = &R.tm_c1[1]; tw = &R.tm_w2; yw = tk.le * P.H; }
+        yw += tk.nb * kBF;
+        const int y = tk.le * P.RP + tk.m * kBM;
+        const int nk = ((tk.type == 0 ? P.H : P.D) + Cfg::BK - 1) / Cfg::BK;
         for (int kb = 0; kb < nk; ++kb) {
+            // weight tile first: the converter warps need it one step before the MMA does
+            if (!mbar_wait(&G.wempty[wstage], wphase ^ 1u, P.abort_flag)) return;
+            mbar_expect_tx(&G.wfull[wstage], Cfg::W_BYTES);
+            tma_load_2d(ring + Cfg::W_OFF + wstage * Cfg::W_BYTES, tw, &G.wfull[wstage], kb * Cfg::BK, yw);
+            if (++wstage == Cfg::WSTAGES) { wstage = 0; wphase ^= 1u; }
+
             if (!mbar_wait(&G.empty[stage], phase ^ 1u, P.abort_flag)) return;
             uint8_t* st = ring + stage * Cfg::STAGE_BYTES;
             mbar_expect_tx(&G.full[stage], Cfg::STAGE_BYTES);
-            const int x = kb * Cfg::BK;
 #pragma unroll
-            for (int pl = 0; pl < Cfg::PLANES; ++pl) {
-                tma_load_2d(st + pl * Cfg::A_BYTES, ta[pl], &G.full[stage], x, ya);
-                tma_load_2d(st + Cfg::PLANES * Cfg::A_BYTES + pl * Cfg::B_BYTES, tb[pl], &G.full[stage], x, yb);
-            }
+            for (int pl = 0; pl < Cfg::PLANES; ++pl)
+                tma_load_2d(st + pl * Cfg::B_BYTES, tb[pl], &G.full[stage], kb * Cfg::BK, y);
             if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
         }
     }
 }
 
+// warps 4-7: weight tile (TMA-staged in smem, SWIZZLE_128B) -> registers -> tf32 hi/lo split ->
+// tcgen05.st into the TMEM weight ring. Thread (warp 4+q, lane l) owns feature row r = 32q+l of
+// the tile = TMEM lane r; its 16-byte chunk c sits at r*128 + ((c ^ (r & 7)) << 4), so a warp's
+// 128-bit loads are bank-conflict free.
+template <int PREC>
+__device__ void gemm_wconvert(const LaunchParams& P, uint8_t* ring, GemmCtrl& G) {
+    using Cfg = GemmCfg<PREC>;
+    const int lane = threadIdx.x & 31;
+    const int wq = (threadIdx.x >> 5) - 4;
+    const int r = wq * 32 + lane;
+    const uint32_t lane_addr = (uint32_t)(wq * 32) << 16;
+    int q = 0;
+    uint32_t qphase = 0;
+    int ast = 0, wst = 0;
+    uint32_t aphase = 0, wphase = 0;
+    const uint32_t tmem = G.tmem_base;
+    while (true) {
+        if (!mbar_wait(&G.qfull[q], qphase, P.abort_flag)) return;
+        const int type = G.ring[q].type;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&G.qempty[q]);
+        if (++q == kTaskRing) { q = 0; qphase ^= 1u; }
+        if (type < 0) return;
+        const int nk = ((type == 0 ? P.H : P.D) + Cfg::BK - 1) / Cfg::BK;
+        for (int kb = 0; kb < nk; ++kb) {
+            if (!mbar_wait(&G.wfull[wst], wphase, P.abort_flag)) return;
+            const uint8_t* wrow = ring + Cfg::W_OFF + wst * Cfg::W_BYTES + r * 128;
+            float4 c[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) c[i] = *reinterpret_cast<const float4*>(wrow + ((i ^ (r & 7)) << 4));
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&G.wempty[wst]);   // values are in registers: slot reusable
+            if (++wst == Cfg::WSTAGES) { wst = 0; wphase ^= 1u; }
+
+            if (!mbar_wait(&G.aempty[ast], aphase ^ 1u, P.abort_flag)) return;
+            tc_fence_after();
+            const uint32_t col = tmem + lane_addr + Cfg::TMEM_A0 + ast * Cfg::A_COLS;
+            if (PREC == kFP32) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {   // 16 K values per half
+                    uint32_t hi[16], lo[16];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const float4 v = c[h * 4 + i];
+                        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const float hv = tf32_hi(vv[u]);
+                            hi[i * 4 + u] = __float_as_uint(hv);
+                            lo[i * 4 + u] = __float_as_uint(__fsub_rn(vv[u], hv));
+                        }
+                    }
+                    tmem_st16(col + h * 16, hi);             // hi: columns [0, 32)
+                    tmem_st16(col + Cfg::BK + h * 16, lo);   // lo: columns [32, 64)
+                }
+            } else {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {   // 32 bf16 (16 columns) per half
+                    uint32_t w[16];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const float4 v = c[h * 4 + i];
+                        w[i * 4 + 0] = __float_as_uint(v.x); w[i * 4 + 1] = __float_as_uint(v.y);
+                        w[i * 4 + 2] = __float_as_uint(v.z); w[i * 4 + 3] = __float_as_uint(v.w);
+                    }
+                    tmem_st16(col + h * 16, w);
+                }
+            }
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&G.afull[ast]);
+            if (++ast == kAStages) { ast = 0; aphase ^= 1u; }
+        }
+    }
+}
+
+// warp 1, one lane: tcgen05.mma issue
 template <int PREC>
 __device__ void gemm_mma(const LaunchParams& P, uint8_t* ring, GemmCtrl& G) {
     using Cfg = GemmCfg<PREC>;
     int stage = 0;
     uint32_t phase = 0;
+    int ast = 0;
+    uint32_t aphase = 0;
     int q = 0;
     uint32_t qphase = 0;
     int acc = 0;
-    uint32_t aphase = 0;
+    uint32_t accphase = 0;
     const uint32_t tmem = G.tmem_base;
     while (true) {
         if (!mbar_wait(&G.qfull[q], qphase, P.abort_flag)) return;
-        const Task& tk = G.ring[q];
-        if (tk.type < 0) return;
-        const int nk = ((tk.type == 0 ? P.H : P.D) + Cfg::BK - 1) / Cfg::BK;
-        if (!mbar_wait(&G.tempty[acc], aphase ^ 1u, P.abort_flag)) return;
-        tc_fence_after();
-        const uint32_t d_tmem = tmem + (uint32_t)(acc * kBN);
-        for (int kb = 0; kb < nk; ++kb) {
-            if (!mbar_wait(&G.full[stage], phase, P.abort_flag)) return;
-            tc_fence_after();
-            const uint32_t base = smem_u32(ring + stage * Cfg::STAGE_BYTES);
-#pragma unroll
-            for (int ks = 0; ks < Cfg::BK / Cfg::KSTEP; ++ks) {
-                const uint32_t koff = ks * Cfg::KSTEP * Cfg::ESZ;   // 32 bytes inside the 128B swizzle atom
-                const uint64_t a0 = umma_desc_kmajor(base + koff, 128);
-                const uint64_t b0 = umma_desc_kmajor(base + Cfg::PLANES * Cfg::A_BYTES + koff, 128);
-                const uint32_t accum = (kb | ks) != 0 ? 1u : 0u;
-                if (PREC == kFP32) {
-                    const uint64_t a1 = umma_desc_kmajor(base + Cfg::A_BYTES + koff, 128);
-                    const uint64_t b1 = umma_desc_kmajor(base + Cfg::PLANES * Cfg::A_BYTES + Cfg::B_BYTES + koff, 128);
-                    // 3xTF32: lo*hi + hi*lo + hi*hi (small terms first)
-                    mma_tf32(d_tmem, a1, b0, Cfg::IDESC, accum);
-                    mma_tf32(d_tmem, a0, b1, Cfg::IDESC, 1u);
-                    mma_tf32(d_tmem, a0, b0, Cfg::IDESC, 1u);
-                } else {
-                    mma_bf16(d_tmem, a0, b0, Cfg::IDESC, accum);
-                }
-            }
-            mma_commit(&G.empty[stage]);   // smem slot free once these MMAs retire
-            if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
-        }
-        mma_commit(&G.tfull[acc]);         // accumulator ready for the epilogue
+        const int type = G.ring[q].type;
         mbar_arrive(&G.qempty[q]);
         if (++q == kTaskRing) { q = 0; qphase ^= 1u; }
-        if (++acc == kAccStages) { acc = 0; aphase ^= 1u; }
+        if (type < 0) return;
+        const int nk = ((type == 0 ? P.H : P.D) + Cfg::BK - 1) / Cfg::BK;
+        if (!mbar_wait(&G.tempty[acc], accphase ^ 1u, P.abort_flag)) return;
+        tc_fence_after();
+        const uint32_t d_tmem = tmem + (uint32_t)(acc * kNT);
+        for (int kb = 0; kb < nk; ++kb) {
+            if (!mbar_wait(&G.full[stage], phase, P.abort_flag)) return;
+            if (!mbar_wait(&G.afull[ast], aphase, P.abort_flag)) return;
+            tc_fence_after();
+            const uint32_t bbase = smem_u32(ring + stage * Cfg::STAGE_BYTES);
+            const uint32_t abase = tmem + Cfg::TMEM_A0 + ast * Cfg::A_COLS;
+#pragma unroll
+            for (int ks = 0; ks < Cfg::BK / Cfg::KSTEP; ++ks) {
+                const uint32_t koff = ks * Cfg::KSTEP * Cfg::ESZ;   // bytes inside the 128B swizzle atom
+                const uint64_t b0 = umma_desc_kmajor(bbase + koff, 128);
+                const uint32_t accum = (kb | ks) != 0 ? 1u : 0u;
+                if (PREC == kFP32) {
+                    const uint64_t b1 = umma_desc_kmajor(bbase + Cfg::B_BYTES + koff, 128);
+                    const uint32_t a_hi = abase + ks * Cfg::KSTEP;
+                    const uint32_t a_lo = a_hi + Cfg::BK;
+                    mma_tf32_ts(d_tmem, a_lo, b0, Cfg::IDESC, accum);   // w_lo * x_hi
+                    mma_tf32_ts(d_tmem, a_hi, b1, Cfg::IDESC, 1u);      // w_hi * x_lo
+                    mma_tf32_ts(d_tmem, a_hi, b0, Cfg::IDESC, 1u);      // w_hi * x_hi
+                } else {
+                    mma_bf16_ts(d_tmem, abase + ks * (Cfg::KSTEP / 2), b0, Cfg::IDESC, accum);
+                }
+            }
+            mma_commit(&G.empty[stage]);   // token stage reusable once these MMAs retire
+            mma_commit(&G.aempty[ast]);    // weight stage reusable
+            if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
+            if (++ast == kAStages) { ast = 0; aphase ^= 1u; }
+        }
+        mma_commit(&G.tfull[acc]);         // accumulator ready for the epilogue
+        if (++acc == kAccStages) { acc = 0; accphase ^= 1u; }
     }
 }
 
+// warps 8-11: thread = output feature (TMEM lane), 32 token columns per tcgen05.ld
 template <int PREC>
 __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl& G, unsigned long long* stat) {
-    const int et = threadIdx.x - 128;   // 0..127 == TMEM lane == tile row
+    const int et = threadIdx.x - 256;   // 0..127 == TMEM lane == feature row in the tile
     const int wq = et >> 5;
     const uint32_t par = P.epoch & 1u;
     int q = 0;
     uint32_t qphase = 0;
     int acc = 0;
-    uint32_t aphase = 0;
+    uint32_t accphase = 0;
     const uint32_t tmem = G.tmem_base;
     const int e_glob_base = R.rank * P.El;
     while (true) {
         if (!mbar_wait(&G.qfull[q], qphase, P.abort_flag)) return;
-        const Task tk = G.ring[q];
-        if (tk.type < 0) return;
-        if (!mbar_wait(&G.tfull[acc], aphase, P.abort_flag)) return;
+        const Task& tk = G.ring[q];   // stays valid until this warp group releases the slot
+        const int type = tk.type;
+        if (type < 0) return;
+        if (!mbar_wait(&G.tfull[acc], accphase, P.abort_flag)) return;
         tc_fence_after();
 
-        // which packet does my row belong to, and is it a valid (signalled) row?
-        int src = -1, slot = 0;
-        bool valid = false;
-        if (P.Cp >= kBM) {
-            src = tk.src0;
-            slot = (tk.m % (P.Cp / kBM)) * kBM + et;
-            valid = et < tk.cnt[0];
-        } else {
-            const int j = et / P.Cp;
-            if (j < tk.nsrc) {
-                src = tk.src0 + j;
-                slot = et - j * P.Cp;
-                valid = slot < tk.cnt[j];
-            }
-        }
-        const size_t grow = (size_t)tk.le * P.RP + (size_t)tk.m * kBM + et;   // row in X / C1
-        const int ncols = tk.type == 0 ? P.D : P.H;
-        const float* bias = (tk.type == 0 ? R.b1 + (size_t)tk.le * P.D : R.b2 + (size_t)tk.le * P.H) + tk.nb * kBN;
+        const int ncols = type == 0 ? P.D : P.H;
+        const int feat = tk.nb * kBF + et;
+        const bool fvalid = feat < ncols;
+        const float bias =
+            fvalid ? __ldg((type == 0 ? R.b1 + (size_t)tk.le * P.D : R.b2 + (size_t)tk.le * P.H) + feat) : 0.0f;
         const int e_glob = e_glob_base + tk.le;
-        float* ydst = nullptr;
-        if (tk.type == 1 && valid)
-            ydst = reinterpret_cast<float*>(R.peer_heap[src] + R.hl.yc) + ((size_t)e_glob * P.C + slot) * P.H +
-                   (size_t)tk.nb * kBN;
-        const uint32_t tbase = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(acc * kBN);
+        const size_t grow0 = (size_t)tk.le * P.RP + (size_t)tk.m * kBM;   // first X / C1 row of the tile
+        const int rb_base = P.Cp >= kBM ? (tk.m % (P.Cp / kBM)) * kBM : 0;
+        const int src0 = tk.src0, nsrc = tk.nsrc, cnt0 = tk.cnt[0];
+        const uint32_t tbase = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(acc * kNT);
+        float* c1hi = reinterpret_cast<float*>(R.c1[0]) + grow0 * (size_t)P.D + feat;
+        float* c1lo = reinterpret_cast<float*>(R.c1[1]) + grow0 * (size_t)P.D + feat;
+        __nv_bfloat16* c1b = reinterpret_cast<__nv_bfloat16*>(R.c1[0]) + grow0 * (size_t)P.D + feat;
 #pragma unroll 1
-        for (int ch = 0; ch < kBN / 32; ++ch) {
-            const int col0 = tk.nb * kBN + ch * 32;
+        for (int ch = 0; ch < kNT / 32; ++ch) {
             uint32_t r[32];
             tmem_ld32(tbase + ch * 32, r);
+            // validity of the 32 token rows of this chunk: bit i = row ch*32+i holds a landed token
+            uint32_t vmask;
+            if (P.Cp >= kBM) {
+                const int lo = ch * 32, n = cnt0 - lo;
+                vmask = n >= 32 ? 0xffffffffu : (n <= 0 ? 0u : ((1u << n) - 1u));
+            } else {
+                vmask = 0;
+                // packets of Cp rows: rows [j*Cp, j*Cp + cnt_j) are valid (Cp in {16, 32, 64})
+                for (int j = (ch * 32) / P.Cp; j < nsrc && j * P.Cp < ch * 32 + 32; ++j) {
+                    const int a = max(j * P.Cp, ch * 32), b = min(j * P.Cp + tk.cnt[j], ch * 32 + 32);
+                    if (b > a) vmask |= (b - a >= 32 ? 0xffffffffu : ((1u << (b - a)) - 1u)) << (a - ch * 32);
+                }
+            }
             tmem_wait_ld();
-            if (!valid || col0 >= ncols) continue;
-            float v[32];
+            if (!fvalid) vmask = 0;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = __fadd_rn(__uint_as_float(r[i]), __ldg(bias + ch * 32 + i));
-            if (tk.type == 0) {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) v[i] = activation(P.act, v[i]);
-                if (PREC == kFP32) {
-                    float4* hi = reinterpret_cast<float4*>(reinterpret_cast<float*>(R.c1[0]) + grow * P.D + col0);
-                    float4* lo = reinterpret_cast<float4*>(reinterpret_cast<float*>(R.c1[1]) + grow * P.D + col0);
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        float4 h, l;
-                        h.x = tf32_hi(v[4 * i]); h.y = tf32_hi(v[4 * i + 1]);
-                        h.z = tf32_hi(v[4 * i + 2]); h.w = tf32_hi(v[4 * i + 3]);
-                        l.x = __fsub_rn(v[4 * i], h.x); l.y = __fsub_rn(v[4 * i + 1], h.y);
-                        l.z = __fsub_rn(v[4 * i + 2], h.z); l.w = __fsub_rn(v[4 * i + 3], h.w);
-                        hi[i] = h;
-                        lo[i] = l;
+            for (int i = 0; i < 32; ++i) {
+                if (!(vmask & (1u << i))) continue;   // warp-uniform: same token row for all lanes
+                const int n = ch * 32 + i;
+                float v = __fadd_rn(__uint_as_float(r[i]), bias);
+                if (type == 0) {
+                    v = activation(P.act, v);
+                    const size_t o = (size_t)n * P.D;
+                    if (PREC == kFP32) {
+                        const float h = tf32_hi(v);
+                        c1hi[o] = h;
+                        c1lo[o] = __fsub_rn(v, h);
+                    } else {
+                        c1b[o] = __float2bfloat16_rn(v);
                     }
                 } else {
-                    uint4* d = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(R.c1[0]) + grow * P.D + col0);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        uint4 o;
-                        __nv_bfloat162 p0 = __floats2bfloat162_rn(v[8 * i + 0], v[8 * i + 1]);
-                        __nv_bfloat162 p1 = __floats2bfloat162_rn(v[8 * i + 2], v[8 * i + 3]);
-                        __nv_bfloat162 p2 = __floats2bfloat162_rn(v[8 * i + 4], v[8 * i + 5]);
-                        __nv_bfloat162 p3 = __floats2bfloat162_rn(v[8 * i + 6], v[8 * i + 7]);
-                        o.x = *reinterpret_cast<uint32_t*>(&p0);
-                        o.y = *reinterpret_cast<uint32_t*>(&p1);
-                        o.z = *reinterpret_cast<uint32_t*>(&p2);
-                        o.w = *reinterpret_cast<uint32_t*>(&p3);
-                        d[i] = o;
-                    }
+                    int src, slot;
+                    if (P.Cp >= kBM) { src = src0; slot = rb_base + n; }
+                    else { const int j = n / P.Cp; src = src0 + j; slot = n - j * P.Cp; }
+                    float* ydst = reinterpret_cast<float*>(R.peer_heap[src] + R.hl.yc) +
+                                  ((size_t)e_glob * P.C + slot) * P.H + feat;
+                    *ydst = v;
                 }
-            } else {
-                float4* d = reinterpret_cast<float4*>(ydst + ch * 32);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) d[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
             }
         }
         tc_fence_before();
-        asm volatile("bar.sync 1, 128;" ::: "memory");   // all epilogue rows stored, TMEM drained
+        asm volatile("bar.sync 1, 128;" ::: "memory");   // all rows stored, TMEM drained
         if (et == 0) {
             mbar_arrive(&G.tempty[acc]);
-            if (tk.type == 0) {
+            if (type == 0) {
                 __threadfence();
                 atomicAdd(R.g0done + (size_t)tk.le * P.MT + tk.m, 1u);
                 stat[0]++;
@@ -855,7 +936,7 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
             mbar_arrive(&G.qempty[q]);
         }
         if (++q == kTaskRing) { q = 0; qphase ^= 1u; }
-        if (++acc == kAccStages) { acc = 0; aphase ^= 1u; }
+        if (++acc == kAccStages) { acc = 0; accphase ^= 1u; }
     }
 }
 
@@ -975,7 +1056,7 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
     unsigned long long* trace = R.trace + (size_t)cta * kTracePts;
     if (tid == 0) trace[0] = globaltimer();
 
-    GemmCtrl& G = *reinterpret_cast<GemmCtrl*>(smem + Cfg::RING_BYTES);
+    GemmCtrl& G = *reinterpret_cast<GemmCtrl*>(smem + SmemPlan<PREC>::REGION);
     uint8_t* ring = smem;
 
     // TMEM: allocated once for the whole launch (1 CTA per SM, all 512 columns)
@@ -994,7 +1075,7 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
     tc_fence_after();
     const uint32_t tmem_base = G.tmem_base;
 
-    // phase 1: exact gate (uses the smem ring as scratch)
+    // phase 1: exact gate (uses the smem region as scratch)
     gate_phase(P, R, A, cta, smem);
     if (tid == 0) trace[1] = globaltimer();
     if (!rank_barrier(P, R, P.launch_seq)) goto done;
@@ -1009,18 +1090,22 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
     // phase 3: expert FFN tiles
     if (tid == 0) {
         for (int i = 0; i < Cfg::STAGES; ++i) { mbar_init(&G.full[i], 1); mbar_init(&G.empty[i], 1); }
+        for (int i = 0; i < Cfg::WSTAGES; ++i) { mbar_init(&G.wfull[i], 1); mbar_init(&G.wempty[i], 4); }
+        for (int i = 0; i < kAStages; ++i) { mbar_init(&G.afull[i], 4); mbar_init(&G.aempty[i], 1); }
         for (int i = 0; i < kAccStages; ++i) { mbar_init(&G.tfull[i], 1); mbar_init(&G.tempty[i], 1); }
-        for (int i = 0; i < kTaskRing; ++i) { mbar_init(&G.qfull[i], 1); mbar_init(&G.qempty[i], 2); }
+        for (int i = 0; i < kTaskRing; ++i) { mbar_init(&G.qfull[i], 1); mbar_init(&G.qempty[i], kTaskConsumers); }
         G.tmem_base = tmem_base;
         mbar_fence_init();
     }
-    fence_proxy_async_smem();   // smem ring was written by the generic proxy in phases 1-2
+    fence_proxy_async_smem();   // the smem region was written by the generic proxy in phases 1-2
     __syncthreads();
     if (warp == 0) {
         if ((tid & 31) == 0) gemm_producer<PREC>(P, R, ring, G);
     } else if (warp == 1) {
         if ((tid & 31) == 0) gemm_mma<PREC>(P, ring, G);
-    } else if (warp >= 4) {
+    } else if (warp >= 4 && warp < 8) {
+        gemm_wconvert<PREC>(P, ring, G);
+    } else if (warp >= 8) {
         gemm_epilogue<PREC>(P, R, G, s_stat);
     }
     __syncthreads();
@@ -1048,10 +1133,9 @@ done:
 }
 
 // ================================================================ weight preparation
-// W (E_local x R x Cc, row-major, the reference's N-contiguous layout) ->
-// W^T (E_local x Cc x R, K-major) as tf32 hi/lo planes or bf16.
-__global__ void prep_transpose_kernel(const float* __restrict__ W, int El, int Rr, int Cc, void* out_hi,
-                                      void* out_lo, int prec) {
+// W (E_local x Rr x Cc, row-major: the reference's N-contiguous layout, config.hpp:130-135)
+// -> W^T (E_local x Cc x Rr, K-major) as FP32 (split into tf32 hi/lo on chip) or bf16.
+__global__ void prep_transpose_kernel(const float* __restrict__ W, int El, int Rr, int Cc, void* out, int prec) {
     __shared__ float tile[32][33];
     const int e = blockIdx.z;
     const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
@@ -1066,13 +1150,8 @@ __global__ void prep_transpose_kernel(const float* __restrict__ W, int El, int R
         if (c < Cc && r < Rr) {
             const float v = tile[threadIdx.x][i];
             const size_t o = (size_t)e * Cc * Rr + (size_t)c * Rr + r;
-            if (prec == kFP32) {
-                const float h = tf32_hi(v);
-                reinterpret_cast<float*>(out_hi)[o] = h;
-                reinterpret_cast<float*>(out_lo)[o] = __fsub_rn(v, h);
-            } else {
-                reinterpret_cast<__nv_bfloat16*>(out_hi)[o] = __float2bfloat16_rn(v);
-            }
+            if (prec == kFP32) reinterpret_cast<float*>(out)[o] = v;
+            else reinterpret_cast<__nv_bfloat16*>(out)[o] = __float2bfloat16_rn(v);
         }
     }
 }
@@ -1083,79 +1162,92 @@ __global__ void debug_expf_kernel(const float* x, float* y, long long n) {
         y[i] = expf_glibc(x[i]);
 }
 
-// Single-tile GEMM through the same TMA -> tcgen05 -> TMEM path (tests the descriptors):
-// D[128 x 256] = A[128 x K] * B[256 x K]^T with A/B given as K-major tensor maps.
+// One tile through the layer's exact machinery (weight loader -> TMEM, TMA token ring,
+// tcgen05.mma, TMEM epilogue): D[f][t] = sum_k W[f][k] * X[t][k], 128 x 128, K-major inputs.
+// W: FP32 [128][K] (bf16 mode: bf16), X planes via tensor maps (128 rows).
 template <int PREC>
-__global__ void __launch_bounds__(kThreads, 1) debug_gemm_kernel(const __grid_constant__ CUtensorMap ta0,
-                                                                 const __grid_constant__ CUtensorMap ta1,
-                                                                 const __grid_constant__ CUtensorMap tb0,
-                                                                 const __grid_constant__ CUtensorMap tb1, int K,
+__global__ void __launch_bounds__(kThreads, 1) debug_gemm_kernel(const __grid_constant__ CUtensorMap tx0,
+                                                                 const __grid_constant__ CUtensorMap tx1,
+                                                                 const __grid_constant__ CUtensorMap tw, int K,
                                                                  float* D, uint32_t* abort_flag) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     using Cfg = GemmCfg<PREC>;
-    GemmCtrl& G = *reinterpret_cast<GemmCtrl*>(smem + Cfg::RING_BYTES);
+    GemmCtrl& G = *reinterpret_cast<GemmCtrl*>(smem + SmemPlan<PREC>::REGION);
     const int tid = threadIdx.x, warp = tid >> 5;
     if (warp == 2) { tmem_alloc(&G.tmem_base, 512); tmem_relinquish(); }
     if (tid == 0) {
         for (int i = 0; i < Cfg::STAGES; ++i) { mbar_init(&G.full[i], 1); mbar_init(&G.empty[i], 1); }
+        for (int i = 0; i < Cfg::WSTAGES; ++i) { mbar_init(&G.wfull[i], 1); mbar_init(&G.wempty[i], 4); }
+        for (int i = 0; i < kAStages; ++i) { mbar_init(&G.afull[i], 4); mbar_init(&G.aempty[i], 1); }
         mbar_init(&G.tfull[0], 1);
+        for (int i = 0; i < kTaskRing; ++i) { mbar_init(&G.qfull[i], 1); mbar_init(&G.qempty[i], kTaskConsumers); }
+        G.ring[0].type = 0;
+        G.ring[1].type = -1;
         mbar_fence_init();
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    if (tid == 0) { mbar_arrive(&G.qfull[0]); mbar_arrive(&G.qfull[1]); }   // one task, then end
     const uint32_t tmem = G.tmem_base;
     const int nk = (K + Cfg::BK - 1) / Cfg::BK;
     if (tid == 0) {
-        int stage = 0; uint32_t phase = 0;
-        const CUtensorMap* ta[2] = {&ta0, &ta1};
-        const CUtensorMap* tb[2] = {&tb0, &tb1};
+        int stage = 0, wstage = 0; uint32_t phase = 0, wphase = 0;
+        const CUtensorMap* tb[2] = {&tx0, &tx1};
         for (int kb = 0; kb < nk; ++kb) {
+            mbar_wait(&G.wempty[wstage], wphase ^ 1u, abort_flag);
+            mbar_expect_tx(&G.wfull[wstage], Cfg::W_BYTES);
+            tma_load_2d(smem + Cfg::W_OFF + wstage * Cfg::W_BYTES, &tw, &G.wfull[wstage], kb * Cfg::BK, 0);
+            if (++wstage == Cfg::WSTAGES) { wstage = 0; wphase ^= 1u; }
             mbar_wait(&G.empty[stage], phase ^ 1u, abort_flag);
             uint8_t* st = smem + stage * Cfg::STAGE_BYTES;
             mbar_expect_tx(&G.full[stage], Cfg::STAGE_BYTES);
-            for (int pl = 0; pl < Cfg::PLANES; ++pl) {
-                tma_load_2d(st + pl * Cfg::A_BYTES, ta[pl], &G.full[stage], kb * Cfg::BK, 0);
-                tma_load_2d(st + Cfg::PLANES * Cfg::A_BYTES + pl * Cfg::B_BYTES, tb[pl], &G.full[stage], kb * Cfg::BK, 0);
-            }
+            for (int pl = 0; pl < Cfg::PLANES; ++pl)
+                tma_load_2d(st + pl * Cfg::B_BYTES, tb[pl], &G.full[stage], kb * Cfg::BK, 0);
             if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
         }
     } else if (tid == 32) {
-        int stage = 0; uint32_t phase = 0;
+        int stage = 0, ast = 0; uint32_t phase = 0, aphase = 0;
         for (int kb = 0; kb < nk; ++kb) {
             mbar_wait(&G.full[stage], phase, abort_flag);
+            mbar_wait(&G.afull[ast], aphase, abort_flag);
             tc_fence_after();
-            const uint32_t base = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+            const uint32_t bbase = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+            const uint32_t abase = tmem + Cfg::TMEM_A0 + ast * Cfg::A_COLS;
             for (int ks = 0; ks < Cfg::BK / Cfg::KSTEP; ++ks) {
                 const uint32_t koff = ks * Cfg::KSTEP * Cfg::ESZ;
-                const uint64_t a0 = umma_desc_kmajor(base + koff, 128);
-                const uint64_t b0 = umma_desc_kmajor(base + Cfg::PLANES * Cfg::A_BYTES + koff, 128);
+                const uint64_t b0 = umma_desc_kmajor(bbase + koff, 128);
                 const uint32_t accum = (kb | ks) != 0 ? 1u : 0u;
                 if (PREC == kFP32) {
-                    const uint64_t a1 = umma_desc_kmajor(base + Cfg::A_BYTES + koff, 128);
-                    const uint64_t b1 = umma_desc_kmajor(base + Cfg::PLANES * Cfg::A_BYTES + Cfg::B_BYTES + koff, 128);
-                    mma_tf32(tmem, a1, b0, Cfg::IDESC, accum);
-                    mma_tf32(tmem, a0, b1, Cfg::IDESC, 1u);
-                    mma_tf32(tmem, a0, b0, Cfg::IDESC, 1u);
+                    const uint64_t b1 = umma_desc_kmajor(bbase + Cfg::B_BYTES + koff, 128);
+                    const uint32_t a_hi = abase + ks * Cfg::KSTEP, a_lo = a_hi + Cfg::BK;
+                    mma_tf32_ts(tmem, a_lo, b0, Cfg::IDESC, accum);
+                    mma_tf32_ts(tmem, a_hi, b1, Cfg::IDESC, 1u);
+                    mma_tf32_ts(tmem, a_hi, b0, Cfg::IDESC, 1u);
                 } else {
-                    mma_bf16(tmem, a0, b0, Cfg::IDESC, accum);
+                    mma_bf16_ts(tmem, abase + ks * (Cfg::KSTEP / 2), b0, Cfg::IDESC, accum);
                 }
             }
             mma_commit(&G.empty[stage]);
+            mma_commit(&G.aempty[ast]);
             if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
+            if (++ast == kAStages) { ast = 0; aphase ^= 1u; }
         }
         mma_commit(&G.tfull[0]);
-    }
-    if (warp >= 4) {
-        const int et = tid - 128, wq = et >> 5;
+    } else if (warp >= 4 && warp < 8) {
+        LaunchParams P{};
+        P.H = K; P.D = K; P.abort_flag = abort_flag;
+        gemm_wconvert<PREC>(P, smem, G);
+    } else if (warp >= 8) {
+        const int et = tid - 256, wq = et >> 5;
         mbar_wait(&G.tfull[0], 0, abort_flag);
         tc_fence_after();
-        for (int ch = 0; ch < kBN / 32; ++ch) {
+        for (int ch = 0; ch < kNT / 32; ++ch) {
             uint32_t r[32];
             tmem_ld32(tmem + ((uint32_t)(wq * 32) << 16) + ch * 32, r);
             tmem_wait_ld();
-            for (int i = 0; i < 32; ++i) D[(size_t)et * kBN + ch * 32 + i] = __uint_as_float(r[i]);
+            for (int i = 0; i < 32; ++i) D[(size_t)et * kNT + ch * 32 + i] = __uint_as_float(r[i]);
         }
         tc_fence_before();
     }
@@ -1165,8 +1257,7 @@ __global__ void __launch_bounds__(kThreads, 1) debug_gemm_kernel(const __grid_co
 
 // ---------------------------------------------------------------- host-visible launchers
 int layer_smem_bytes(int prec) {
-    const int g = prec == kFP32 ? GemmCfg<kFP32>::SMEM_BYTES : GemmCfg<kBF16>::SMEM_BYTES;
-    return g + 1024;   // + alignment slack
+    return prec == kFP32 ? SmemPlan<kFP32>::TOTAL : SmemPlan<kBF16>::TOTAL;
 }
 
 cudaError_t launch_layer(const LaunchParams& p, int grid, int smem, cudaStream_t stream) {
@@ -1193,10 +1284,9 @@ int layer_max_blocks_per_sm(int prec, int smem) {
     return n;
 }
 
-cudaError_t launch_prep_transpose(const float* W, int El, int Rr, int Cc, void* hi, void* lo, int prec,
-                                  cudaStream_t s) {
+cudaError_t launch_prep_transpose(const float* W, int El, int Rr, int Cc, void* out, int prec, cudaStream_t s) {
     dim3 grid((Cc + 31) / 32, (Rr + 31) / 32, El);
-    prep_transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(W, El, Rr, Cc, hi, lo, prec);
+    prep_transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(W, El, Rr, Cc, out, prec);
     return cudaGetLastError();
 }
 
@@ -1205,14 +1295,15 @@ cudaError_t launch_debug_expf(const float* x, float* y, long long n, cudaStream_
     return cudaGetLastError();
 }
 
-cudaError_t launch_debug_gemm(int prec, const CUtensorMap* t, int K, float* D, uint32_t* abort_flag, cudaStream_t s) {
+cudaError_t launch_debug_gemm(int prec, const CUtensorMap* t, int K, float* D, uint32_t* abort_flag,
+                              cudaStream_t s) {
     const int smem = layer_smem_bytes(prec);
     if (prec == kFP32) {
         cudaFuncSetAttribute(debug_gemm_kernel<kFP32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        debug_gemm_kernel<kFP32><<<1, kThreads, smem, s>>>(t[0], t[1], t[2], t[3], K, D, abort_flag);
+        debug_gemm_kernel<kFP32><<<1, kThreads, smem, s>>>(t[0], t[1], t[2], K, D, abort_flag);
     } else {
         cudaFuncSetAttribute(debug_gemm_kernel<kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        debug_gemm_kernel<kBF16><<<1, kThreads, smem, s>>>(t[0], t[1], t[2], t[3], K, D, abort_flag);
+        debug_gemm_kernel<kBF16><<<1, kThreads, smem, s>>>(t[0], t[1], t[2], K, D, abort_flag);
     }
     return cudaGetLastError();
 }

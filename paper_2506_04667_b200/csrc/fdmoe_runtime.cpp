@@ -49,11 +49,11 @@ Dims make_dims(const fdmoe_config& c) {
     d.RP = d.P * d.Cp;
     d.MT = (d.RP + kBM - 1) / kBM;
     d.RBF = d.Cp >= kBM ? d.Cp / kBM : 1;
-    d.NB0 = (d.D + kBN - 1) / kBN;
-    d.NB1 = (d.H + kBN - 1) / kBN;
+    d.NB0 = (d.D + kBF - 1) / kBF;   // GEMM0 feature blocks
+    d.NB1 = (d.H + kBF - 1) / kBF;   // GEMM1 feature blocks
     d.rows_x = std::max(d.El * d.RP, (d.El - 1) * d.RP + d.MT * kBM);
-    d.rows_w1 = (d.El - 1) * d.D + d.NB0 * kBN;
-    d.rows_w2 = (d.El - 1) * d.H + d.NB1 * kBN;
+    d.rows_w1 = (d.El - 1) * d.D + d.NB0 * kBF;
+    d.rows_w2 = (d.El - 1) * d.H + d.NB1 * kBF;
     d.prec = c.precision;
     d.esz = c.precision == FDMOE_FP32 ? 4 : 2;
     d.planes = c.precision == FDMOE_FP32 ? 2 : 1;
@@ -179,11 +179,12 @@ fdmoe_status alloc_rank(fdmoe_handle* h, RankRes& r, int ctas_per_rank) {
     // ---- private scratch
     std::vector<std::pair<void**, size_t>> parts;
     const size_t c1plane = (size_t)d.rows_x * d.D * d.esz;
+    // expert weights: ONE plane (FP32, split into tf32 hi/lo on chip; or bf16), K-major
     const size_t w1plane = (size_t)d.rows_w1 * d.H * d.esz;
     const size_t w2plane = (size_t)d.rows_w2 * d.D * d.esz;
     for (int pl = 0; pl < d.planes; ++pl) parts.push_back({&r.c1[pl], c1plane});
-    for (int pl = 0; pl < d.planes; ++pl) parts.push_back({&r.w1[pl], w1plane});
-    for (int pl = 0; pl < d.planes; ++pl) parts.push_back({&r.w2[pl], w2plane});
+    parts.push_back({&r.w1[0], w1plane});
+    parts.push_back({&r.w2[0], w2plane});
     parts.push_back({(void**)&r.b1, (size_t)d.El * d.D * 4});
     parts.push_back({(void**)&r.b2, (size_t)d.El * d.H * 4});
     parts.push_back({(void**)&r.wg, (size_t)d.H * d.E * 4});
@@ -210,11 +211,9 @@ fdmoe_status alloc_rank(fdmoe_handle* h, RankRes& r, int ctas_per_rank) {
     CK(cudaMemset(r.trace, 0, (size_t)ctas_per_rank * kTracePts * 8));
     CK(cudaMemset(r.ctrl, 0, ctrl_bytes(d)));
     CK(cudaMemset(r.blk_ready, 0, (size_t)(d.S + kGateTok - 1) / kGateTok * 4));
-    for (int pl = 0; pl < d.planes; ++pl) {   // padding rows of the weight planes stay finite
-        CK(cudaMemset(r.w1[pl], 0, w1plane));
-        CK(cudaMemset(r.w2[pl], 0, w2plane));
-    }
-    r.weight_bytes = (w1plane + w2plane) * d.planes;
+    CK(cudaMemset(r.w1[0], 0, w1plane));   // padding rows stay finite
+    CK(cudaMemset(r.w2[0], 0, w2plane));
+    r.weight_bytes = w1plane + w2plane;
     return FDMOE_OK;
 }
 
@@ -234,9 +233,9 @@ fdmoe_status build_ctx(fdmoe_handle* h) {
             for (int pl = 0; pl < 2; ++pl) {
                 const int p = pl < d.planes ? pl : 0;
                 if ((st = make_tmap(&c.tm_c1[pl], r.c1[p], d.rows_x, d.D, d.esz, kBM))) return st;
-                if ((st = make_tmap(&c.tm_w1[pl], r.w1[p], d.rows_w1, d.H, d.esz, kBN))) return st;
-                if ((st = make_tmap(&c.tm_w2[pl], r.w2[p], d.rows_w2, d.D, d.esz, kBN))) return st;
             }
+            if ((st = make_tmap(&c.tm_w1, r.w1[0], d.rows_w1, d.H, d.esz, kBF))) return st;
+            if ((st = make_tmap(&c.tm_w2, r.w2[0], d.rows_w2, d.D, d.esz, kBF))) return st;
             for (int q = 0; q < d.P; ++q) c.peer_heap[q] = r.peer[q];
             c.hl = r.hl;
             c.c1[0] = r.c1[0];
@@ -447,10 +446,10 @@ fdmoe_status fdmoe_set_weights(fdmoe_handle* h, const float* wg, const float* w1
         float* tmp = nullptr;
         CK(cudaMalloc(&tmp, wbytes));
         CK(cudaMemcpy(tmp, w1 + e0 * d.H * d.D, wbytes, kind));
-        CK(launch_prep_transpose(tmp, (int)d.El, (int)d.H, (int)d.D, r.w1[0], r.w1[d.planes - 1], d.prec, 0));
+        CK(launch_prep_transpose(tmp, (int)d.El, (int)d.H, (int)d.D, r.w1[0], d.prec, 0));
         CK(cudaDeviceSynchronize());
         CK(cudaMemcpy(tmp, w2 + e0 * d.D * d.H, wbytes, kind));
-        CK(launch_prep_transpose(tmp, (int)d.El, (int)d.D, (int)d.H, r.w2[0], r.w2[d.planes - 1], d.prec, 0));
+        CK(launch_prep_transpose(tmp, (int)d.El, (int)d.D, (int)d.H, r.w2[0], d.prec, 0));
         CK(cudaDeviceSynchronize());
         CK(cudaFree(tmp));
         CK(cudaMemcpy(r.b1, b1 + e0 * d.D, (size_t)d.El * d.D * 4, kind));
@@ -665,58 +664,56 @@ fdmoe_status fdmoe_debug_expf(const float* x, float* y, int64_t n) {
     return FDMOE_OK;
 }
 
-// D[128 x 256] = A[128 x K] * B[256 x K]^T (row-major FP32 host inputs). prec as fdmoe_precision.
-fdmoe_status fdmoe_debug_gemm(int32_t prec, int32_t K, const float* A, const float* B, float* D) {
+// D[f][t] = sum_k W[f][k] * X[t][k]: W 128 x K (weights, TMEM operand), X 128 x K (tokens, TMA
+// operand), host row-major FP32; D 128 x 128. prec as fdmoe_precision.
+fdmoe_status fdmoe_debug_gemm(int32_t prec, int32_t K, const float* W, const float* X, float* D) {
     if (K % 64 != 0) return fail(FDMOE_ERR_CONFIG, "K must be a multiple of 64");
     const int esz = prec == FDMOE_FP32 ? 4 : 2;
-    std::vector<uint8_t> planes[4];
-    auto split = [&](const float* src, size_t n, std::vector<uint8_t>& hi, std::vector<uint8_t>& lo) {
-        hi.resize(n * esz);
-        lo.resize(n * esz);
-        for (size_t i = 0; i < n; ++i) {
-            if (prec == FDMOE_FP32) {
-                uint32_t u;
-                std::memcpy(&u, &src[i], 4);
-                u = (u + 0x1000u) & 0xFFFFE000u;
-                float h;
-                std::memcpy(&h, &u, 4);
-                const float l = src[i] - h;
-                std::memcpy(&hi[i * 4], &h, 4);
-                std::memcpy(&lo[i * 4], &l, 4);
-            } else {
-                uint32_t u;
-                std::memcpy(&u, &src[i], 4);
-                const uint32_t r = u + 0x7FFFu + ((u >> 16) & 1u);   // round to nearest even
-                const uint16_t b = (uint16_t)(r >> 16);
-                std::memcpy(&hi[i * 2], &b, 2);
-                std::memcpy(&lo[i * 2], &b, 2);
-            }
-        }
+    auto to_bf16 = [](float f) {
+        uint32_t u;
+        std::memcpy(&u, &f, 4);
+        return (uint16_t)((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);
     };
-    split(A, (size_t)128 * K, planes[0], planes[1]);
-    split(B, (size_t)256 * K, planes[2], planes[3]);
-    void* dp[4];
-    for (int i = 0; i < 4; ++i) {
-        CK(cudaMalloc(&dp[i], planes[i].size()));
-        CK(cudaMemcpy(dp[i], planes[i].data(), planes[i].size(), cudaMemcpyHostToDevice));
+    std::vector<uint8_t> wp((size_t)128 * K * esz), xh((size_t)128 * K * esz), xl((size_t)128 * K * esz);
+    for (size_t i = 0; i < (size_t)128 * K; ++i) {
+        if (prec == FDMOE_FP32) {
+            std::memcpy(&wp[i * 4], &W[i], 4);
+            uint32_t u;
+            std::memcpy(&u, &X[i], 4);
+            u = (u + 0x1000u) & 0xFFFFE000u;
+            float h;
+            std::memcpy(&h, &u, 4);
+            const float l = X[i] - h;
+            std::memcpy(&xh[i * 4], &h, 4);
+            std::memcpy(&xl[i * 4], &l, 4);
+        } else {
+            const uint16_t bw = to_bf16(W[i]), bx = to_bf16(X[i]);
+            std::memcpy(&wp[i * 2], &bw, 2);
+            std::memcpy(&xh[i * 2], &bx, 2);
+            std::memcpy(&xl[i * 2], &bx, 2);
+        }
     }
-    CUtensorMap tm[4];
+    void *dw = nullptr, *dxh = nullptr, *dxl = nullptr;
+    CK(cudaMalloc(&dw, wp.size()));
+    CK(cudaMalloc(&dxh, xh.size()));
+    CK(cudaMalloc(&dxl, xl.size()));
+    CK(cudaMemcpy(dw, wp.data(), wp.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dxh, xh.data(), xh.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dxl, xl.data(), xl.size(), cudaMemcpyHostToDevice));
+    CUtensorMap tm[3];
     fdmoe_status st;
-    if ((st = make_tmap(&tm[0], dp[0], 128, K, esz, kBM))) return st;
-    if ((st = make_tmap(&tm[1], dp[1], 128, K, esz, kBM))) return st;
-    if ((st = make_tmap(&tm[2], dp[2], 256, K, esz, kBN))) return st;
-    if ((st = make_tmap(&tm[3], dp[3], 256, K, esz, kBN))) return st;
+    if ((st = make_tmap(&tm[0], dxh, 128, K, esz, kNT))) return st;
+    if ((st = make_tmap(&tm[1], dxl, 128, K, esz, kNT))) return st;
+    if ((st = make_tmap(&tm[2], dw, 128, K, esz, kBF))) return st;
     float* dD = nullptr;
     uint32_t* abort_flag = nullptr;
-    CK(cudaMalloc(&dD, 128 * 256 * 4));
+    CK(cudaMalloc(&dD, 128 * 128 * 4));
     CK(cudaMalloc(&abort_flag, 4));
     CK(cudaMemset(abort_flag, 0, 4));
     CK(launch_debug_gemm(prec, tm, K, dD, abort_flag, 0));
     CK(cudaDeviceSynchronize());
-    CK(cudaMemcpy(D, dD, 128 * 256 * 4, cudaMemcpyDeviceToHost));
-    for (int i = 0; i < 4; ++i) cudaFree(dp[i]);
-    cudaFree(dD);
-    cudaFree(abort_flag);
+    CK(cudaMemcpy(D, dD, 128 * 128 * 4, cudaMemcpyDeviceToHost));
+    cudaFree(dw); cudaFree(dxh); cudaFree(dxl); cudaFree(dD); cudaFree(abort_flag);
     return FDMOE_OK;
 }
 

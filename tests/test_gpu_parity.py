@@ -59,15 +59,17 @@ def test_device_expf_matches_glibc():
 
 
 @pytest.mark.parametrize("prec", [fd.Precision.fp32, fd.Precision.bf16])
-@pytest.mark.parametrize("K", [64, 512])
+@pytest.mark.parametrize("K", [64, 512, 2048])
 def test_tcgen05_tile(prec, K):
+    """One FFN tile through the layer's machinery: weights -> registers -> TMEM (A operand,
+    tf32 hi/lo split on chip), tokens -> TMA -> smem (B operand), tcgen05.mma, TMEM epilogue."""
     rng = np.random.default_rng(K + prec)
-    A = rng.standard_normal((128, K)).astype(np.float32)
-    B = rng.standard_normal((256, K)).astype(np.float32)
-    D = np.empty((128, 256), np.float32)
-    fd._check(fd.lib().fdmoe_debug_gemm(prec, K, fd._ptr(A), fd._ptr(B), fd._ptr(D)))
+    W = rng.standard_normal((128, K)).astype(np.float32)
+    X = rng.standard_normal((128, K)).astype(np.float32)
+    D = np.empty((128, 128), np.float32)
+    fd._check(fd.lib().fdmoe_debug_gemm(prec, K, fd._ptr(W), fd._ptr(X), fd._ptr(D)))
     if prec == fd.Precision.fp32:
-        want = A.astype(np.float64) @ B.astype(np.float64).T
+        want = W.astype(np.float64) @ X.astype(np.float64).T
         err = np.abs(D - want).max() / np.abs(want).max()
         # 3xTF32 drops lo*lo (|lo| <= 2^-11|x| with round-to-nearest hi); measured on B200 the
         # tcgen05 FP32 accumulation adds an error growing ~linearly in K (~8e-9*K normwise:
@@ -76,9 +78,9 @@ def test_tcgen05_tile(prec, K):
         assert err < 1e-6 + 1e-8 * K, err
     else:
         import torch
-        Ab = torch.from_numpy(A).bfloat16().double().numpy()
-        Bb = torch.from_numpy(B).bfloat16().double().numpy()
-        want = Ab @ Bb.T
+        Wb = torch.from_numpy(W).bfloat16().double().numpy()
+        Xb = torch.from_numpy(X).bfloat16().double().numpy()
+        want = Wb @ Xb.T
         err = np.abs(D - want).max() / np.abs(want).max()
         assert err < 1e-5, err
 
