@@ -188,9 +188,13 @@ fdmoe_status fdmoe_get_info(fdmoe_handle* h, fdmoe_info* info);
  * max over this handle's devices). Call after fdmoe_sync / fdmoe_forward. */
 fdmoe_status fdmoe_last_kernel_ms(fdmoe_handle* h, double* ms);
 /* Device trace of the most recent launch (the reference's TraceBuffer role, trace.hpp:17-118, at
- * phase granularity): per CTA of local rank `local_rank`, 8 u64 = %globaltimer ns at kernel start,
- * gate done, grid barrier passed, dispatch done, FFN tiles done, combine done, exit; then the number
- * of FFN tiles that CTA executed. Writes min(cap/8, ctas) rows; *n_ctas = CTAs of that rank. */
+ * phase granularity): per CTA of local rank `local_rank`, 20 u64 = %globaltimer ns at kernel start,
+ * gate done, grid barrier passed, dispatch done, FFN tiles done, combine done, exit; the number of
+ * FFN tiles that CTA executed; then SM cycles blocked per FFN pipeline edge: MMA<-tokens,
+ * MMA<-weights, MMA<-accumulator, converter<-weight TMA, converter<-TMEM stage, producer<-weight
+ * slot, producer<-token slot, epilogue<-accumulator, MMA<-task ring; producer cycles fetching and
+ * resolving tiles; epilogue busy cycles; FFN tiles issued by the MMA warp.
+ * Writes min(cap/20, ctas) rows, then clears. */
 fdmoe_status fdmoe_read_trace(fdmoe_handle* h, int32_t local_rank, uint64_t* out, int32_t cap, int32_t* n_ctas);
 
 /* ---- diagnostics (tests only; not part of the reference surface) -------------------- */
@@ -200,6 +204,16 @@ fdmoe_status fdmoe_debug_expf(const float* x, float* y, int64_t n);
  * token rows via TMA -> smem operand, tcgen05.mma, TMEM epilogue):
  * D[f][t] = sum_k W[f][k] * X[t][k]; W, X: 128 x K host row-major FP32 (K % 64 == 0). */
 fdmoe_status fdmoe_debug_gemm(int32_t precision, int32_t K, const float* W, const float* X, float* D);
+/* Issue-rate microbenchmark: SM cycles per tcgen05.mma (M=128, A from TMEM, N in {64,128,256})
+ * when `nissuers` warps (1-2) each issue `iters` back-to-back MMAs into their own accumulator;
+ * kind 0 = tf32, 1 = bf16. */
+/* Latency probe (cycles): [0] issue of n tf32 N=128 MMAs, [1] issue -> commit completion,
+ * [2] 8 x tcgen05.st.x16 + wait::st, [3] mbarrier wait with a 2000-cycle delayed arrive. */
+fdmoe_status fdmoe_debug_latency(int32_t n, uint64_t* out4);
+/* Debug: CTA 0's MMA-warp chunk timeline of the last launch (512 x {clock, wait tokens,
+ * wait weights, issue}); enabled when FDMOE_CHUNKLOG is set at fdmoe_create. */
+fdmoe_status fdmoe_read_chunklog(fdmoe_handle* h, uint64_t* out);
+fdmoe_status fdmoe_debug_mma_rate(int32_t kind, int32_t nissuers, int32_t N, int32_t iters, double* cycles_per_mma);
 
 #ifdef __cplusplus
 }

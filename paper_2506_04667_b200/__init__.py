@@ -117,7 +117,7 @@ EXPORTED_SYMBOLS = [
     "fdmoe_gemm_tasks_for_rows", "fdmoe_combine_tiles_for_rows", "fdmoe_initial_task_bound",
     "fdmoe_synth_model", "fdmoe_synth_shards", "fdmoe_create", "fdmoe_destroy", "fdmoe_ipc_size",
     "fdmoe_export_heap", "fdmoe_import_peers", "fdmoe_set_weights", "fdmoe_forward", "fdmoe_forward_async",
-    "fdmoe_sync", "fdmoe_get_info", "fdmoe_last_kernel_ms", "fdmoe_read_trace", "fdmoe_debug_expf", "fdmoe_debug_gemm",
+    "fdmoe_sync", "fdmoe_get_info", "fdmoe_last_kernel_ms", "fdmoe_read_trace", "fdmoe_debug_expf", "fdmoe_debug_gemm", "fdmoe_debug_mma_rate", "fdmoe_debug_latency", "fdmoe_read_chunklog",
 ]
 
 _LIB = None
@@ -165,6 +165,9 @@ def lib():
         "fdmoe_read_trace": (i32, [vp, i32, vp, i32, vp]),
         "fdmoe_debug_expf": (i32, [f32p, f32p, i64]),
         "fdmoe_debug_gemm": (i32, [i32, i32, f32p, f32p, f32p]),
+        "fdmoe_debug_mma_rate": (i32, [i32, i32, i32, i32, vp]),
+        "fdmoe_debug_latency": (i32, [i32, vp]),
+        "fdmoe_read_chunklog": (i32, [vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -508,7 +511,7 @@ class Operator:
         """Per-CTA phase timestamps of the last launch (ns, relative to the earliest CTA start):
         columns start, gate, barrier, dispatch, ffn, combine, end, ffn_tiles."""
         info = self.info()
-        buf = np.zeros((info["ctas_per_rank"], 8), np.uint64)
+        buf = np.zeros((info["ctas_per_rank"], 20), np.uint64)
         n = C.c_int32()
         _check(lib().fdmoe_read_trace(self._h, local_rank, _ptr(buf), buf.size, C.byref(n)))
         t = buf.astype(np.int64)

@@ -8,10 +8,12 @@
 namespace fdmoe {
 
 // ---------------------------------------------------------------- constants
-// 12 warps: w0 tile scheduler + TMA (token operand), w1 tcgen05.mma issuer, w2 TMEM allocator,
-// w3 spare, w4-7 weight loaders (global -> registers -> tf32 hi/lo split -> TMEM),
-// w8-11 epilogue (TMEM -> registers -> bias/activation -> global / peer stores)
+// 12 warps. FFN roles: w0-3 epilogue (TMEM -> registers -> bias/activation -> global / peer
+// stores), w4-7 weight converters (TMA-staged smem -> registers -> tf32 hi/lo -> TMEM), w8 TMEM
+// allocator, w10 tile scheduler + TMA producer, w11 tcgen05.mma issuer (the warp arbiter favours
+// high warp ids, so the single-lane issuers sit on top).
 constexpr int kThreads = 384;
+constexpr int kWarpConv0 = 4, kWarpTmem = 8, kWarpProducer = 10, kWarpMma = 11;
 constexpr int kBM = 128;            // tokens per row tile of an expert's receive region
 constexpr int kBF = 128;            // output features per FFN tile (MMA M = TMEM lanes)
 constexpr int kNT = 128;            // tokens per FFN tile (MMA N = accumulator columns)
@@ -26,7 +28,13 @@ constexpr int kMaxRanks = 64;       // P envelope (peer table size)
 constexpr int kMaxSrcPerTile = 8;   // packet_rows >= 16 -> <= 8 packets per 128-row tile
 constexpr int kCombineTok = 16;     // tokens per combine task (== kGateTok)
 constexpr int kMaxLocalRanks = 8;   // ranks per launch (virtual ranks on one GPU)
-constexpr int kTracePts = 8;        // start, gate, barrier, dispatch, gemm, combine, end, tiles
+constexpr int kTracePts = 20;
+constexpr int kChunkLog = 512;       // start, gate, barrier, dispatch, gemm, combine, end, tiles,
+                                    // then FFN pipeline wait cycles (see kWait*)
+enum WaitSlot : int {
+    kWaitMmaX = 8, kWaitMmaA, kWaitMmaAcc, kWaitConvW, kWaitConvA, kWaitProdW, kWaitProdX, kWaitEpiAcc,
+    kWaitMmaTask, kProdFetch, kEpiBusy, kMmaTiles
+};
 
 enum Prec : int { kFP32 = 0, kBF16 = 1 };
 
@@ -73,6 +81,7 @@ struct alignas(64) RankCtx {
     uint32_t* err;             // [4] error word: code, where, a, b
     unsigned long long* stats; // [8] gemm0, gemm1, combine tasks, dispatch rows, ...
     unsigned long long* trace; // [ctas][kTracePts] %globaltimer per phase boundary (device trace)
+    unsigned long long* chunklog;   // debug: CTA 0 MMA-warp chunk timeline [kChunkLog][4] (null = off)
     int32_t rank;
 };
 
@@ -89,6 +98,14 @@ struct LaunchParams {
     unsigned long long budget_ns;    // watchdog budget
     uint32_t* abort_flag;      // per launch-group abort word
     int sequential;            // bulk-synchronous schedule (grid barrier after each phase)
+    int debug;                 // ablation bits (FDMOE_DEBUG env; 0 in production): see kDbg*
+};
+enum DebugBits : int {
+    kDbgNoConvert = 1,    // converter warps skip the split + tcgen05.st (MMA reads stale TMEM)
+    kDbgOneProduct = 2,   // issue only the hi*hi product
+    kDbgNoEpiStore = 4,   // epilogue skips global stores
+    kDbgNoXTma = 8,       // producer skips the token TMA (barrier completes without data)
+    kDbgNoWTma = 16,      // producer skips the weight TMA
 };
 
 // Error codes written to RankCtx::err[0] (mirrors the reference's exceptions).
@@ -99,6 +116,7 @@ enum DevErr : uint32_t { kErrNone = 0, kErrTimeout = 1, kErrProtocol = 2, kErrAc
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+__device__ __forceinline__ long long clk() { return clock64(); }
 __device__ __forceinline__ uint64_t globaltimer() {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

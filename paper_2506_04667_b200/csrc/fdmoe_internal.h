@@ -21,4 +21,7 @@ cudaError_t launch_debug_expf(const float* x, float* y, long long n, cudaStream_
 cudaError_t launch_debug_gemm(int prec, const CUtensorMap* t, int K, float* D, uint32_t* abort_flag,
                               cudaStream_t s);
 
+cudaError_t launch_debug_latency(int n, unsigned long long* out);
+cudaError_t launch_debug_mma_rate(int kind, int N, int iters, int nissuers, unsigned long long* out);
+
 }  // namespace fdmoe

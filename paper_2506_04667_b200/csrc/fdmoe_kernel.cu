@@ -550,26 +550,36 @@ struct Task {
     int cnt[kMaxSrcPerTile];   // valid rows per packet in the tile
 };
 
+// Stage = BK elements of K = NATOM SWIZZLE_128B atoms (128-byte rows). One wait + one commit per
+// stage: ready[s] completes when the token TMA bytes landed AND the 4 converter warps stored the
+// weight stage into TMEM; done[s] is committed by the MMA warp when the stage's MMAs retire.
+// (The tensor queue is ~1 instruction deep, so per-stage bookkeeping is paid as a bubble; a stage
+// carries 24 MMAs in FP32 mode.)
 template <int PREC>
 struct GemmCfg {
-    static constexpr int BK = PREC == kFP32 ? 32 : 64;          // K per stage: 128-byte rows (SWIZZLE_128B)
     static constexpr int ESZ = PREC == kFP32 ? 4 : 2;
-    static constexpr int B_BYTES = kNT * BK * ESZ;             // one token-operand plane per stage
-    static constexpr int PLANES = PREC == kFP32 ? 2 : 1;       // hi/lo split of the token operand
-    static constexpr int STAGE_BYTES = B_BYTES * PLANES;
-    static constexpr int STAGES = 4;                            // token ring
-    static constexpr int W_BYTES = kBF * BK * ESZ;             // weight tile per stage (raw FP32 / bf16)
-    static constexpr int WSTAGES = PREC == kFP32 ? 4 : 6;      // weight ring (TMA -> smem -> TMEM)
+    static constexpr int ATOM_K = 128 / ESZ;                    // K elements per 128-byte atom row
+    static constexpr int NATOM = 2;
+    static constexpr int BK = ATOM_K * NATOM;                   // K per stage (64 fp32 / 128 bf16)
+    static constexpr int ATOM_BYTES = 128 * 128;                // 128 rows x 128 B
+    static constexpr int PLANE_BYTES = ATOM_BYTES * NATOM;      // one operand plane per stage (32 KB)
+    static constexpr int PLANES = PREC == kFP32 ? 2 : 1;        // hi/lo split of the token operand
+    static constexpr int STAGE_BYTES = PLANE_BYTES * PLANES;   // token stage
+    static constexpr int STAGES = PREC == kFP32 ? 2 : 3;       // token smem ring == weight TMEM ring
+    static constexpr int W_BYTES = PLANE_BYTES;                 // weight stage (raw FP32 / bf16)
+    static constexpr int WSTAGES = PREC == kFP32 ? 2 : 3;      // weight smem ring (TMA -> converters)
     static constexpr int KSTEP = PREC == kFP32 ? 8 : 16;       // K per tcgen05.mma
+    static constexpr int KSTEPS = BK / KSTEP;                   // 8
+    static constexpr int STEPS_PER_ATOM = ATOM_K / KSTEP;       // 4
     static constexpr int A_COLS = PREC == kFP32 ? 2 * BK : BK / 2;   // TMEM columns per weight stage
     static constexpr uint32_t IDESC = umma_idesc(PREC == kFP32 ? 2u : 1u, kBF, kNT);
     static constexpr int W_OFF = STAGE_BYTES * STAGES;
     static constexpr int RING_BYTES = W_OFF + W_BYTES * WSTAGES;
     static constexpr uint32_t TMEM_A0 = kAccStages * kNT;      // first weight-stage column
-    static_assert(TMEM_A0 + kAStages * A_COLS <= 512, "TMEM budget");
+    static_assert(TMEM_A0 + STAGES * A_COLS <= 512, "TMEM budget");
 };
 
-// dynamic smem: [max(gate scratch, token ring)] [GemmCtrl]
+// dynamic smem: [max(gate scratch, FFN rings)] [GemmCtrl]
 template <int PREC>
 struct SmemPlan {
     static constexpr int REGION = ((kGateSmemBytes > GemmCfg<PREC>::RING_BYTES ? kGateSmemBytes
@@ -579,16 +589,16 @@ struct SmemPlan {
 };
 
 struct GemmCtrl {
-    uint64_t full[8], empty[8];                      // token-operand smem ring
-    uint64_t wfull[8], wempty[8];                    // weight smem ring
-    uint64_t afull[kAStages], aempty[kAStages];      // weight-operand TMEM ring
+    uint64_t ready[4], done[4];                      // token smem ring + weight TMEM ring (same stages)
+    uint64_t wfull[4], wempty[4];                    // weight smem ring (producer -> converters)
     uint64_t tfull[kAccStages], tempty[kAccStages];  // accumulators
     uint64_t qfull[kTaskRing], qempty[kTaskRing];    // task ring
     uint32_t tmem_base;
     uint32_t pad;
     Task ring[kTaskRing];
 };
-constexpr int kTaskConsumers = 1 + 4 + 1;   // MMA warp, 4 loader warps, epilogue
+constexpr int kTaskConsumers = 1 + 4 + 1;   // MMA warp, 4 converter warps, epilogue
+constexpr int kReadyCount = 1 + 4;          // producer (expect_tx) + 4 converter warps
 
 __device__ __forceinline__ void decode_task(const LaunchParams& P, uint32_t t, uint32_t n_g0, Task& tk) {
     const bool g1 = t >= n_g0;
@@ -635,10 +645,21 @@ __device__ int resolve_tile_rows(const LaunchParams& P, const RankCtx& R, Task& 
     return total;
 }
 
+// Wait accounting (device trace slots 8..15): cycles each role spends blocked on a pipeline edge.
+#define FD_TIMED_WAIT(acc, expr)              \
+    ({                                        \
+        const long long _t0 = clk();          \
+        const bool _ok = (expr);              \
+        acc += clk() - _t0;                   \
+        _ok;                                  \
+    })
+
 // warp 0, one lane: fetch tiles, resolve dependencies, stream the token operand
 template <int PREC>
-__device__ void gemm_producer(const LaunchParams& P, const RankCtx& R, uint8_t* ring, GemmCtrl& G) {
+__device__ void gemm_producer(const LaunchParams& P, const RankCtx& R, uint8_t* ring, GemmCtrl& G,
+                              unsigned long long* trace) {
     using Cfg = GemmCfg<PREC>;
+    long long w_w = 0, w_x = 0, t_fetch = 0;
     const uint32_t n_g0 = (uint32_t)P.El * P.NB0 * P.MT;
     const uint32_t n_g1 = (uint32_t)P.El * P.NB1 * P.MT;
     const uint32_t par = P.epoch & 1u;
@@ -653,6 +674,7 @@ __device__ void gemm_producer(const LaunchParams& P, const RankCtx& R, uint8_t* 
     tma_prefetch(&R.tm_w1);
     tma_prefetch(&R.tm_w2);
     while (true) {
+        const long long tf0 = clk();
         const uint32_t t = atomicAdd(R.gemm_head, 1u);
         Task tk;
         bool end = t >= n_g0 + n_g1;
@@ -665,10 +687,14 @@ __device__ void gemm_producer(const LaunchParams& P, const RankCtx& R, uint8_t* 
                 if (!wait_counter(P, R, R.g0done + (size_t)tk.le * P.MT + tk.m, (uint32_t)P.NB0, 302)) end = true;
             }
         }
+        t_fetch += clk() - tf0;
         if (!mbar_wait(&G.qempty[q], qphase ^ 1u, P.abort_flag)) end = true;
         if (end) {
             G.ring[q].type = -1;
             mbar_arrive(&G.qfull[q]);
+            trace[kWaitProdW] = w_w;
+            trace[kWaitProdX] = w_x;
+            trace[kProdFetch] = t_fetch;
             return;
         }
         G.ring[q] = tk;
@@ -688,17 +714,29 @@ __device__ void gemm_producer(const LaunchParams& P, const RankCtx& R, uint8_t* 
         const int nk = ((tk.type == 0 ? P.H : P.D) + Cfg::BK - 1) / Cfg::BK;
         for (int kb = 0; kb < nk; ++kb) {
             // weight tile first: the converter warps need it one step before the MMA does
-            if (!mbar_wait(&G.wempty[wstage], wphase ^ 1u, P.abort_flag)) return;
-            mbar_expect_tx(&G.wfull[wstage], Cfg::W_BYTES);
-            tma_load_2d(ring + Cfg::W_OFF + wstage * Cfg::W_BYTES, tw, &G.wfull[wstage], kb * Cfg::BK, yw);
+            if (!FD_TIMED_WAIT(w_w, mbar_wait(&G.wempty[wstage], wphase ^ 1u, P.abort_flag))) return;
+            if (P.debug & kDbgNoWTma) mbar_arrive(&G.wfull[wstage]);
+            else {
+                mbar_expect_tx(&G.wfull[wstage], Cfg::W_BYTES);
+#pragma unroll
+                for (int at = 0; at < Cfg::NATOM; ++at)
+                    tma_load_2d(ring + Cfg::W_OFF + wstage * Cfg::W_BYTES + at * Cfg::ATOM_BYTES, tw,
+                                &G.wfull[wstage], kb * Cfg::BK + at * Cfg::ATOM_K, yw);
+            }
             if (++wstage == Cfg::WSTAGES) { wstage = 0; wphase ^= 1u; }
 
-            if (!mbar_wait(&G.empty[stage], phase ^ 1u, P.abort_flag)) return;
+            if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.done[stage], phase ^ 1u, P.abort_flag))) return;
             uint8_t* st = ring + stage * Cfg::STAGE_BYTES;
-            mbar_expect_tx(&G.full[stage], Cfg::STAGE_BYTES);
+            if (P.debug & kDbgNoXTma) mbar_arrive(&G.ready[stage]);
+            else {
+                mbar_expect_tx(&G.ready[stage], Cfg::STAGE_BYTES);
 #pragma unroll
-            for (int pl = 0; pl < Cfg::PLANES; ++pl)
-                tma_load_2d(st + pl * Cfg::B_BYTES, tb[pl], &G.full[stage], kb * Cfg::BK, y);
+                for (int pl = 0; pl < Cfg::PLANES; ++pl)
+#pragma unroll
+                    for (int at = 0; at < Cfg::NATOM; ++at)
+                        tma_load_2d(st + pl * Cfg::PLANE_BYTES + at * Cfg::ATOM_BYTES, tb[pl], &G.ready[stage],
+                                    kb * Cfg::BK + at * Cfg::ATOM_K, y);
+            }
             if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
         }
     }
@@ -706,13 +744,14 @@ __device__ void gemm_producer(const LaunchParams& P, const RankCtx& R, uint8_t* 
 
 // warps 4-7: weight tile (TMA-staged in smem, SWIZZLE_128B) -> registers -> tf32 hi/lo split ->
 // tcgen05.st into the TMEM weight ring. Thread (warp 4+q, lane l) owns feature row r = 32q+l of
-// the tile = TMEM lane r; its 16-byte chunk c sits at r*128 + ((c ^ (r & 7)) << 4), so a warp's
-// 128-bit loads are bank-conflict free.
+// the tile = TMEM lane r; in atom a its 16-byte chunk c sits at a*16K + r*128 + ((c ^ (r & 7)) << 4),
+// so a warp's 128-bit loads are bank-conflict free.
 template <int PREC>
-__device__ void gemm_wconvert(const LaunchParams& P, uint8_t* ring, GemmCtrl& G) {
+__device__ void gemm_wconvert(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, unsigned long long* trace) {
     using Cfg = GemmCfg<PREC>;
+    long long w_w = 0, w_a = 0;
     const int lane = threadIdx.x & 31;
-    const int wq = (threadIdx.x >> 5) - 4;
+    const int wq = (threadIdx.x >> 5) - kWarpConv0;
     const int r = wq * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(wq * 32) << 16;
     int q = 0;
@@ -726,110 +765,151 @@ __device__ void gemm_wconvert(const LaunchParams& P, uint8_t* ring, GemmCtrl& G)
         __syncwarp();
         if (lane == 0) mbar_arrive(&G.qempty[q]);
         if (++q == kTaskRing) { q = 0; qphase ^= 1u; }
-        if (type < 0) return;
+        if (type < 0) {
+            if (threadIdx.x == kWarpConv0 * 32 && trace) { trace[kWaitConvW] = w_w; trace[kWaitConvA] = w_a; }
+            return;
+        }
         const int nk = ((type == 0 ? P.H : P.D) + Cfg::BK - 1) / Cfg::BK;
         for (int kb = 0; kb < nk; ++kb) {
-            if (!mbar_wait(&G.wfull[wst], wphase, P.abort_flag)) return;
+            if (!FD_TIMED_WAIT(w_w, mbar_wait(&G.wfull[wst], wphase, P.abort_flag))) return;
             const uint8_t* wrow = ring + Cfg::W_OFF + wst * Cfg::W_BYTES + r * 128;
-            float4 c[8];
+            float4 c[Cfg::NATOM][8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) c[i] = *reinterpret_cast<const float4*>(wrow + ((i ^ (r & 7)) << 4));
+            for (int at = 0; at < Cfg::NATOM; ++at)
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    c[at][i] = *reinterpret_cast<const float4*>(wrow + at * Cfg::ATOM_BYTES + ((i ^ (r & 7)) << 4));
             __syncwarp();
             if (lane == 0) mbar_arrive(&G.wempty[wst]);   // values are in registers: slot reusable
             if (++wst == Cfg::WSTAGES) { wst = 0; wphase ^= 1u; }
 
-            if (!mbar_wait(&G.aempty[ast], aphase ^ 1u, P.abort_flag)) return;
+            if (!FD_TIMED_WAIT(w_a, mbar_wait(&G.done[ast], aphase ^ 1u, P.abort_flag))) return;
             tc_fence_after();
             const uint32_t col = tmem + lane_addr + Cfg::TMEM_A0 + ast * Cfg::A_COLS;
-            if (PREC == kFP32) {
+            if (P.debug & kDbgNoConvert) {
+            } else if (PREC == kFP32) {
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {   // 16 K values per half
-                    uint32_t hi[16], lo[16];
+                for (int at = 0; at < Cfg::NATOM; ++at)
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const float4 v = c[h * 4 + i];
-                        const float vv[4] = {v.x, v.y, v.z, v.w};
+                    for (int h = 0; h < 2; ++h) {   // 16 K values per half atom
+                        uint32_t hi[16], lo[16];
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const float hv = tf32_hi(vv[u]);
-                            hi[i * 4 + u] = __float_as_uint(hv);
-                            lo[i * 4 + u] = __float_as_uint(__fsub_rn(vv[u], hv));
+                        for (int i = 0; i < 4; ++i) {
+                            const float4 v = c[at][h * 4 + i];
+                            const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const float hv = tf32_hi(vv[u]);
+                                hi[i * 4 + u] = __float_as_uint(hv);
+                                lo[i * 4 + u] = __float_as_uint(__fsub_rn(vv[u], hv));
+                            }
                         }
+                        const int k0 = at * Cfg::ATOM_K + h * 16;
+                        tmem_st16(col + k0, hi);             // hi: columns [0, BK)
+                        tmem_st16(col + Cfg::BK + k0, lo);   // lo: columns [BK, 2 BK)
                     }
-                    tmem_st16(col + h * 16, hi);             // hi: columns [0, 32)
-                    tmem_st16(col + Cfg::BK + h * 16, lo);   // lo: columns [32, 64)
-                }
             } else {
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {   // 32 bf16 (16 columns) per half
-                    uint32_t w[16];
+                for (int at = 0; at < Cfg::NATOM; ++at)
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const float4 v = c[h * 4 + i];
-                        w[i * 4 + 0] = __float_as_uint(v.x); w[i * 4 + 1] = __float_as_uint(v.y);
-                        w[i * 4 + 2] = __float_as_uint(v.z); w[i * 4 + 3] = __float_as_uint(v.w);
+                    for (int h = 0; h < 2; ++h) {   // 32 bf16 (16 columns) per half atom
+                        uint32_t w[16];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const float4 v = c[at][h * 4 + i];
+                            w[i * 4 + 0] = __float_as_uint(v.x); w[i * 4 + 1] = __float_as_uint(v.y);
+                            w[i * 4 + 2] = __float_as_uint(v.z); w[i * 4 + 3] = __float_as_uint(v.w);
+                        }
+                        tmem_st16(col + at * 32 + h * 16, w);
                     }
-                    tmem_st16(col + h * 16, w);
-                }
             }
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&G.afull[ast]);
-            if (++ast == kAStages) { ast = 0; aphase ^= 1u; }
+            if (lane == 0) mbar_arrive(&G.ready[ast]);
+            if (++ast == Cfg::STAGES) { ast = 0; aphase ^= 1u; }
         }
     }
 }
 
-// warp 1, one lane: tcgen05.mma issue
+// warp 11, one lane: tcgen05.mma issue. One wait (ready) and one commit (done) per stage.
 template <int PREC>
-__device__ void gemm_mma(const LaunchParams& P, uint8_t* ring, GemmCtrl& G) {
+__device__ __forceinline__ void issue_stage(uint32_t d_tmem, uint32_t abase, uint32_t bbase, int kb, int np) {
     using Cfg = GemmCfg<PREC>;
+    if (PREC == kFP32) {
+        // 3xTF32, PRODUCT-major: back-to-back MMAs that read the same TMEM A columns serialize
+        // (measured 61% of peak k-step-major vs 100% product-major)
+#pragma unroll
+        for (int p = 0; p < 3; ++p) {
+            if (p >= np) break;
+#pragma unroll
+            for (int ks = 0; ks < Cfg::KSTEPS; ++ks) {
+                const uint32_t boff = (ks / Cfg::STEPS_PER_ATOM) * Cfg::ATOM_BYTES +
+                                      (ks % Cfg::STEPS_PER_ATOM) * Cfg::KSTEP * Cfg::ESZ;
+                const uint32_t a_hi = abase + ks * Cfg::KSTEP;
+                const uint32_t accum = (kb | ks | p) != 0 ? 1u : 0u;
+                if (np == 1 || p == 2)   // w_hi * x_hi
+                    mma_tf32_ts(d_tmem, a_hi, umma_desc_kmajor(bbase + boff, 128), Cfg::IDESC, accum);
+                else if (p == 0)         // w_lo * x_hi
+                    mma_tf32_ts(d_tmem, a_hi + Cfg::BK, umma_desc_kmajor(bbase + boff, 128), Cfg::IDESC, accum);
+                else                     // w_hi * x_lo
+                    mma_tf32_ts(d_tmem, a_hi, umma_desc_kmajor(bbase + Cfg::PLANE_BYTES + boff, 128), Cfg::IDESC,
+                                accum);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int ks = 0; ks < Cfg::KSTEPS; ++ks) {
+            const uint32_t boff = (ks / Cfg::STEPS_PER_ATOM) * Cfg::ATOM_BYTES +
+                                  (ks % Cfg::STEPS_PER_ATOM) * Cfg::KSTEP * Cfg::ESZ;
+            mma_bf16_ts(d_tmem, abase + ks * (Cfg::KSTEP / 2), umma_desc_kmajor(bbase + boff, 128), Cfg::IDESC,
+                        (kb | ks) != 0 ? 1u : 0u);
+        }
+    }
+}
+
+template <int PREC>
+__device__ void gemm_mma(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, unsigned long long* trace,
+                         unsigned long long* chunklog) {
+    using Cfg = GemmCfg<PREC>;
+    int nlog = 0;
+    long long w_x = 0, w_acc = 0, w_task = 0, ntile = 0;
     int stage = 0;
     uint32_t phase = 0;
-    int ast = 0;
-    uint32_t aphase = 0;
     int q = 0;
     uint32_t qphase = 0;
     int acc = 0;
     uint32_t accphase = 0;
     const uint32_t tmem = G.tmem_base;
+    const int np = (P.debug & kDbgOneProduct) ? 1 : 3;
     while (true) {
-        if (!mbar_wait(&G.qfull[q], qphase, P.abort_flag)) return;
+        if (!FD_TIMED_WAIT(w_task, mbar_wait(&G.qfull[q], qphase, P.abort_flag))) return;
         const int type = G.ring[q].type;
         mbar_arrive(&G.qempty[q]);
         if (++q == kTaskRing) { q = 0; qphase ^= 1u; }
-        if (type < 0) return;
+        if (type < 0) {
+            trace[kWaitMmaX] = w_x; trace[kWaitMmaA] = 0; trace[kWaitMmaAcc] = w_acc;
+            trace[kWaitMmaTask] = w_task; trace[kMmaTiles] = ntile;
+            return;
+        }
+        ++ntile;
         const int nk = ((type == 0 ? P.H : P.D) + Cfg::BK - 1) / Cfg::BK;
-        if (!mbar_wait(&G.tempty[acc], accphase ^ 1u, P.abort_flag)) return;
+        if (!FD_TIMED_WAIT(w_acc, mbar_wait(&G.tempty[acc], accphase ^ 1u, P.abort_flag))) return;
         tc_fence_after();
         const uint32_t d_tmem = tmem + (uint32_t)(acc * kNT);
         for (int kb = 0; kb < nk; ++kb) {
-            if (!mbar_wait(&G.full[stage], phase, P.abort_flag)) return;
-            if (!mbar_wait(&G.afull[ast], aphase, P.abort_flag)) return;
+            const long long c0 = clk();
+            if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.ready[stage], phase, P.abort_flag))) return;
+            const long long c1 = clk();
             tc_fence_after();
-            const uint32_t bbase = smem_u32(ring + stage * Cfg::STAGE_BYTES);
-            const uint32_t abase = tmem + Cfg::TMEM_A0 + ast * Cfg::A_COLS;
-#pragma unroll
-            for (int ks = 0; ks < Cfg::BK / Cfg::KSTEP; ++ks) {
-                const uint32_t koff = ks * Cfg::KSTEP * Cfg::ESZ;   // bytes inside the 128B swizzle atom
-                const uint64_t b0 = umma_desc_kmajor(bbase + koff, 128);
-                const uint32_t accum = (kb | ks) != 0 ? 1u : 0u;
-                if (PREC == kFP32) {
-                    const uint64_t b1 = umma_desc_kmajor(bbase + Cfg::B_BYTES + koff, 128);
-                    const uint32_t a_hi = abase + ks * Cfg::KSTEP;
-                    const uint32_t a_lo = a_hi + Cfg::BK;
-                    mma_tf32_ts(d_tmem, a_lo, b0, Cfg::IDESC, accum);   // w_lo * x_hi
-                    mma_tf32_ts(d_tmem, a_hi, b1, Cfg::IDESC, 1u);      // w_hi * x_lo
-                    mma_tf32_ts(d_tmem, a_hi, b0, Cfg::IDESC, 1u);      // w_hi * x_hi
-                } else {
-                    mma_bf16_ts(d_tmem, abase + ks * (Cfg::KSTEP / 2), b0, Cfg::IDESC, accum);
-                }
+            issue_stage<PREC>(d_tmem, tmem + Cfg::TMEM_A0 + stage * Cfg::A_COLS,
+                              smem_u32(ring + stage * Cfg::STAGE_BYTES), kb, np);
+            mma_commit(&G.done[stage]);   // token + weight stage reusable once these MMAs retire
+            if (chunklog && nlog < kChunkLog) {
+                unsigned long long* e = chunklog + 4 * nlog++;
+                e[0] = c0; e[1] = c1 - c0; e[2] = 0; e[3] = clk() - c1;
             }
-            mma_commit(&G.empty[stage]);   // token stage reusable once these MMAs retire
-            mma_commit(&G.aempty[ast]);    // weight stage reusable
             if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
-            if (++ast == kAStages) { ast = 0; aphase ^= 1u; }
         }
         mma_commit(&G.tfull[acc]);         // accumulator ready for the epilogue
         if (++acc == kAccStages) { acc = 0; accphase ^= 1u; }
@@ -838,8 +918,10 @@ __device__ void gemm_mma(const LaunchParams& P, uint8_t* ring, GemmCtrl& G) {
 
 // warps 8-11: thread = output feature (TMEM lane), 32 token columns per tcgen05.ld
 template <int PREC>
-__device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl& G, unsigned long long* stat) {
-    const int et = threadIdx.x - 256;   // 0..127 == TMEM lane == feature row in the tile
+__device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl& G, unsigned long long* stat,
+                              unsigned long long* trace) {
+    long long w_acc = 0, busy = 0;
+    const int et = threadIdx.x;   // warps 0-3: 0..127 == TMEM lane == feature row in the tile
     const int wq = et >> 5;
     const uint32_t par = P.epoch & 1u;
     int q = 0;
@@ -852,9 +934,13 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
         if (!mbar_wait(&G.qfull[q], qphase, P.abort_flag)) return;
         const Task& tk = G.ring[q];   // stays valid until this warp group releases the slot
         const int type = tk.type;
-        if (type < 0) return;
-        if (!mbar_wait(&G.tfull[acc], accphase, P.abort_flag)) return;
+        if (type < 0) {
+            if (threadIdx.x == 0) { trace[kWaitEpiAcc] = w_acc; trace[kEpiBusy] = busy; }
+            return;
+        }
+        if (!FD_TIMED_WAIT(w_acc, mbar_wait(&G.tfull[acc], accphase, P.abort_flag))) return;
         tc_fence_after();
+        const long long tb0 = clk();
 
         const int ncols = type == 0 ? P.D : P.H;
         const int feat = tk.nb * kBF + et;
@@ -887,7 +973,7 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
                 }
             }
             tmem_wait_ld();
-            if (!fvalid) vmask = 0;
+            if (!fvalid || (P.debug & kDbgNoEpiStore)) vmask = 0;
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
                 if (!(vmask & (1u << i))) continue;   // warp-uniform: same token row for all lanes
@@ -935,6 +1021,7 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
             }
             mbar_arrive(&G.qempty[q]);
         }
+        busy += clk() - tb0;
         if (++q == kTaskRing) { q = 0; qphase ^= 1u; }
         if (++acc == kAccStages) { acc = 0; accphase ^= 1u; }
     }
@@ -1060,7 +1147,7 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
     uint8_t* ring = smem;
 
     // TMEM: allocated once for the whole launch (1 CTA per SM, all 512 columns)
-    if (warp == 2) {
+    if (warp == kWarpTmem) {
         tmem_alloc(&G.tmem_base, 512);
         tmem_relinquish();
     }
@@ -1089,9 +1176,8 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
 
     // phase 3: expert FFN tiles
     if (tid == 0) {
-        for (int i = 0; i < Cfg::STAGES; ++i) { mbar_init(&G.full[i], 1); mbar_init(&G.empty[i], 1); }
+        for (int i = 0; i < Cfg::STAGES; ++i) { mbar_init(&G.ready[i], kReadyCount); mbar_init(&G.done[i], 1); }
         for (int i = 0; i < Cfg::WSTAGES; ++i) { mbar_init(&G.wfull[i], 1); mbar_init(&G.wempty[i], 4); }
-        for (int i = 0; i < kAStages; ++i) { mbar_init(&G.afull[i], 4); mbar_init(&G.aempty[i], 1); }
         for (int i = 0; i < kAccStages; ++i) { mbar_init(&G.tfull[i], 1); mbar_init(&G.tempty[i], 1); }
         for (int i = 0; i < kTaskRing; ++i) { mbar_init(&G.qfull[i], 1); mbar_init(&G.qempty[i], kTaskConsumers); }
         G.tmem_base = tmem_base;
@@ -1099,14 +1185,16 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
     }
     fence_proxy_async_smem();   // the smem region was written by the generic proxy in phases 1-2
     __syncthreads();
-    if (warp == 0) {
-        if ((tid & 31) == 0) gemm_producer<PREC>(P, R, ring, G);
-    } else if (warp == 1) {
-        if ((tid & 31) == 0) gemm_mma<PREC>(P, ring, G);
-    } else if (warp >= 4 && warp < 8) {
-        gemm_wconvert<PREC>(P, ring, G);
-    } else if (warp >= 8) {
-        gemm_epilogue<PREC>(P, R, G, s_stat);
+    // Role placement follows the warp arbiter (highest warp id first): the single-lane MMA issuer
+    // and TMA producer get the top warp ids so busy converter/epilogue warps cannot starve them.
+    if (warp == kWarpMma) {
+        if ((tid & 31) == 0) gemm_mma<PREC>(P, ring, G, trace, (cta == 0 && R.chunklog) ? R.chunklog : nullptr);
+    } else if (warp == kWarpProducer) {
+        if ((tid & 31) == 0) gemm_producer<PREC>(P, R, ring, G, trace);
+    } else if (warp >= kWarpConv0 && warp < kWarpConv0 + 4) {
+        gemm_wconvert<PREC>(P, ring, G, trace);
+    } else if (warp < 4) {
+        gemm_epilogue<PREC>(P, R, G, s_stat, trace);
     }
     __syncthreads();
     if (tid == 0) trace[4] = globaltimer();
@@ -1121,7 +1209,7 @@ done:
         trace[6] = globaltimer();
         trace[7] = s_stat[0] + s_stat[1];
     }
-    if (warp == 2) {
+    if (warp == kWarpTmem) {
         tc_fence_after();
         tmem_dealloc(tmem_base, 512);
     }
@@ -1175,11 +1263,10 @@ __global__ void __launch_bounds__(kThreads, 1) debug_gemm_kernel(const __grid_co
     using Cfg = GemmCfg<PREC>;
     GemmCtrl& G = *reinterpret_cast<GemmCtrl*>(smem + SmemPlan<PREC>::REGION);
     const int tid = threadIdx.x, warp = tid >> 5;
-    if (warp == 2) { tmem_alloc(&G.tmem_base, 512); tmem_relinquish(); }
+    if (warp == kWarpTmem) { tmem_alloc(&G.tmem_base, 512); tmem_relinquish(); }
     if (tid == 0) {
-        for (int i = 0; i < Cfg::STAGES; ++i) { mbar_init(&G.full[i], 1); mbar_init(&G.empty[i], 1); }
+        for (int i = 0; i < Cfg::STAGES; ++i) { mbar_init(&G.ready[i], kReadyCount); mbar_init(&G.done[i], 1); }
         for (int i = 0; i < Cfg::WSTAGES; ++i) { mbar_init(&G.wfull[i], 1); mbar_init(&G.wempty[i], 4); }
-        for (int i = 0; i < kAStages; ++i) { mbar_init(&G.afull[i], 4); mbar_init(&G.aempty[i], 1); }
         mbar_init(&G.tfull[0], 1);
         for (int i = 0; i < kTaskRing; ++i) { mbar_init(&G.qfull[i], 1); mbar_init(&G.qempty[i], kTaskConsumers); }
         G.ring[0].type = 0;
@@ -1192,55 +1279,42 @@ __global__ void __launch_bounds__(kThreads, 1) debug_gemm_kernel(const __grid_co
     if (tid == 0) { mbar_arrive(&G.qfull[0]); mbar_arrive(&G.qfull[1]); }   // one task, then end
     const uint32_t tmem = G.tmem_base;
     const int nk = (K + Cfg::BK - 1) / Cfg::BK;
-    if (tid == 0) {
+    if (tid == kWarpProducer * 32) {
         int stage = 0, wstage = 0; uint32_t phase = 0, wphase = 0;
         const CUtensorMap* tb[2] = {&tx0, &tx1};
         for (int kb = 0; kb < nk; ++kb) {
             mbar_wait(&G.wempty[wstage], wphase ^ 1u, abort_flag);
             mbar_expect_tx(&G.wfull[wstage], Cfg::W_BYTES);
-            tma_load_2d(smem + Cfg::W_OFF + wstage * Cfg::W_BYTES, &tw, &G.wfull[wstage], kb * Cfg::BK, 0);
+            for (int at = 0; at < Cfg::NATOM; ++at)
+                tma_load_2d(smem + Cfg::W_OFF + wstage * Cfg::W_BYTES + at * Cfg::ATOM_BYTES, &tw, &G.wfull[wstage],
+                            kb * Cfg::BK + at * Cfg::ATOM_K, 0);
             if (++wstage == Cfg::WSTAGES) { wstage = 0; wphase ^= 1u; }
-            mbar_wait(&G.empty[stage], phase ^ 1u, abort_flag);
+            mbar_wait(&G.done[stage], phase ^ 1u, abort_flag);
             uint8_t* st = smem + stage * Cfg::STAGE_BYTES;
-            mbar_expect_tx(&G.full[stage], Cfg::STAGE_BYTES);
+            mbar_expect_tx(&G.ready[stage], Cfg::STAGE_BYTES);
             for (int pl = 0; pl < Cfg::PLANES; ++pl)
-                tma_load_2d(st + pl * Cfg::B_BYTES, tb[pl], &G.full[stage], kb * Cfg::BK, 0);
+                for (int at = 0; at < Cfg::NATOM; ++at)
+                    tma_load_2d(st + pl * Cfg::PLANE_BYTES + at * Cfg::ATOM_BYTES, tb[pl], &G.ready[stage],
+                                kb * Cfg::BK + at * Cfg::ATOM_K, 0);
             if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
         }
-    } else if (tid == 32) {
-        int stage = 0, ast = 0; uint32_t phase = 0, aphase = 0;
+    } else if (tid == kWarpMma * 32) {
+        int stage = 0; uint32_t phase = 0;
         for (int kb = 0; kb < nk; ++kb) {
-            mbar_wait(&G.full[stage], phase, abort_flag);
-            mbar_wait(&G.afull[ast], aphase, abort_flag);
+            mbar_wait(&G.ready[stage], phase, abort_flag);
             tc_fence_after();
-            const uint32_t bbase = smem_u32(smem + stage * Cfg::STAGE_BYTES);
-            const uint32_t abase = tmem + Cfg::TMEM_A0 + ast * Cfg::A_COLS;
-            for (int ks = 0; ks < Cfg::BK / Cfg::KSTEP; ++ks) {
-                const uint32_t koff = ks * Cfg::KSTEP * Cfg::ESZ;
-                const uint64_t b0 = umma_desc_kmajor(bbase + koff, 128);
-                const uint32_t accum = (kb | ks) != 0 ? 1u : 0u;
-                if (PREC == kFP32) {
-                    const uint64_t b1 = umma_desc_kmajor(bbase + Cfg::B_BYTES + koff, 128);
-                    const uint32_t a_hi = abase + ks * Cfg::KSTEP, a_lo = a_hi + Cfg::BK;
-                    mma_tf32_ts(tmem, a_lo, b0, Cfg::IDESC, accum);
-                    mma_tf32_ts(tmem, a_hi, b1, Cfg::IDESC, 1u);
-                    mma_tf32_ts(tmem, a_hi, b0, Cfg::IDESC, 1u);
-                } else {
-                    mma_bf16_ts(tmem, abase + ks * (Cfg::KSTEP / 2), b0, Cfg::IDESC, accum);
-                }
-            }
-            mma_commit(&G.empty[stage]);
-            mma_commit(&G.aempty[ast]);
+            issue_stage<PREC>(tmem, tmem + Cfg::TMEM_A0 + stage * Cfg::A_COLS, smem_u32(smem + stage * Cfg::STAGE_BYTES),
+                              kb, 3);
+            mma_commit(&G.done[stage]);
             if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
-            if (++ast == kAStages) { ast = 0; aphase ^= 1u; }
         }
         mma_commit(&G.tfull[0]);
-    } else if (warp >= 4 && warp < 8) {
+    } else if (warp >= kWarpConv0 && warp < kWarpConv0 + 4) {
         LaunchParams P{};
         P.H = K; P.D = K; P.abort_flag = abort_flag;
-        gemm_wconvert<PREC>(P, smem, G);
-    } else if (warp >= 8) {
-        const int et = tid - 256, wq = et >> 5;
+        gemm_wconvert<PREC>(P, smem, G, nullptr);
+    } else if (warp < 4) {
+        const int et = tid, wq = et >> 5;
         mbar_wait(&G.tfull[0], 0, abort_flag);
         tc_fence_after();
         for (int ch = 0; ch < kNT / 32; ++ch) {
@@ -1252,7 +1326,238 @@ __global__ void __launch_bounds__(kThreads, 1) debug_gemm_kernel(const __grid_co
         tc_fence_before();
     }
     __syncthreads();
-    if (warp == 2) { tc_fence_after(); tmem_dealloc(tmem, 512); }
+    if (warp == kWarpTmem) { tc_fence_after(); tmem_dealloc(tmem, 512); }
+}
+
+// MMA issue-rate microbenchmark: `nissuers` warps (lane 0 each) issue `iters` tcgen05.mma (M=128,
+// A from TMEM, tf32 or bf16) back to back, each into its own accumulator; returns SM cycles for
+// the whole batch / total MMAs (i.e. cycles per MMA per SM).
+template <int KIND, int N>
+__device__ __forceinline__ void mma_burst(uint32_t d, uint32_t a_t, uint64_t b, int iters, int walk) {
+    constexpr uint32_t idesc = umma_idesc(KIND == 0 ? 2u : 1u, 128, N);
+    mma_tf32_ts(d, a_t, b, idesc, 0u);
+    for (int i = 1; i < iters; i += 8) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            // walk = 1: each MMA reads a different B slice (k-step inside the 128B atom, then stage)
+            const uint64_t bb = walk ? b + (uint64_t)(((u & 3) * 32 + (u >> 2) * (N * 128)) >> 4) : b;
+            const uint32_t aa = walk ? a_t + (u & 3) * 8 : a_t;
+            if (KIND == 0) mma_tf32_ts(d, aa, bb, idesc, 1u);
+            else mma_bf16_ts(d, aa, bb, idesc, 1u);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(384, 1) debug_mma_rate_kernel(int kind, int N, int iters, int nissuers,
+                                                                 unsigned long long* out, int walk) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    __shared__ uint32_t s_tmem;
+    __shared__ __align__(8) uint64_t s_bar[4];
+    __shared__ __align__(8) uint64_t s_never;
+    __shared__ volatile int s_stop;
+    __shared__ long long s_t[2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < 160 * 1024 / 4; i += blockDim.x)   // pseudo-random finite data
+        reinterpret_cast<float*>(smem)[i] = walk ? (float)((i * 2654435761u) >> 20) * 1e-3f - 2.0f : 0.0f;
+    if (warp == 0) { tmem_alloc(&s_tmem, 512); tmem_relinquish(); }
+    if (threadIdx.x == 0) { for (int i = 0; i < 4; ++i) mbar_init(&s_bar[i], 1); mbar_init(&s_never, 1); s_stop = 0; mbar_fence_init(); }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = s_tmem;
+    const uint64_t b = umma_desc_kmajor(smem_u32(smem + (walk ? 0 : 32768)), 128);
+    const int spinners = blockDim.x / 32 - 4;   // warps 4.. spin (noise) while warp 0..3 issue
+    if (walk && warp < 4) {   // random tf32/bf16-valid data in the A stages too
+        uint32_t v[16];
+        for (int i = 0; i < 16; ++i) v[i] = __float_as_uint((float)((threadIdx.x * 16 + i) % 7) * 0.25f - 0.7f);
+        for (int c = 0; c < 256; c += 16) tmem_st16(tmem + ((uint32_t)(warp * 32) << 16) + 256 + c, v);
+        tmem_wait_st();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (threadIdx.x == 0) s_t[0] = clock64();
+    __syncthreads();
+    if (warp >= 4 && spinners > 0) {   // polling noise: try_wait on a barrier that never completes
+        while (!s_stop) { mbar_try_wait(&s_never, 0); }
+    }
+    if (warp < nissuers && lane == 0) {
+        const uint32_t d = tmem + (uint32_t)(warp * (N <= 128 ? 128 : 0));
+        const uint32_t a_t = tmem + 256 + warp * 64;
+        if (kind == 0) {
+            if (N == 64) mma_burst<0, 64>(d, a_t, b, iters, walk);
+            else if (N == 128) mma_burst<0, 128>(d, a_t, b, iters, walk);
+            else mma_burst<0, 256>(d, a_t, b, iters, walk);
+        } else {
+            if (N == 64) mma_burst<1, 64>(d, a_t, b, iters, walk);
+            else if (N == 128) mma_burst<1, 128>(d, a_t, b, iters, walk);
+            else mma_burst<1, 256>(d, a_t, b, iters, walk);
+        }
+        mma_commit(&s_bar[warp]);
+        while (!mbar_try_wait(&s_bar[warp], 0)) {}
+        if (warp == 0) out[blockIdx.x] = (unsigned long long)(clock64() - s_t[0]);
+        s_stop = 1;
+    }
+    __syncthreads();
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) { tc_fence_after(); tmem_dealloc(tmem, 512); }
+}
+
+// Latency probe: issue `n` tf32 N=128 MMAs (+commit) and time until the commit's mbarrier fires;
+// also time tcgen05.st (16 columns) + wait::st, and an mbarrier arrive->wait wakeup.
+__global__ void __launch_bounds__(128, 1) debug_latency_kernel(int n, unsigned long long* out) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    __shared__ uint32_t s_tmem;
+    __shared__ __align__(8) uint64_t s_bar[2];
+    const int warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < 32 * 1024 / 4; i += blockDim.x)   // pseudo-random finite operands
+        reinterpret_cast<float*>(smem)[i] = (float)((i * 2654435761u) >> 20) * 1e-3f - 2.0f;
+    if (warp == 0) { tmem_alloc(&s_tmem, 512); tmem_relinquish(); }
+    if (threadIdx.x == 0) { mbar_init(&s_bar[0], 1); mbar_init(&s_bar[1], 1); mbar_fence_init(); }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = s_tmem;
+    if (warp < 4 && n >= 2000) {   // random A operand in TMEM
+        uint32_t v[16];
+        for (int i = 0; i < 16; ++i) v[i] = __float_as_uint((float)(((threadIdx.x * 16 + i) * 2654435761u) >> 22) * 1e-3f - 0.5f);
+        for (int c = 0; c < 256; c += 16) tmem_st16(tmem + ((uint32_t)(warp * 32) << 16) + 256 + c, v);
+        tmem_wait_st();
+        tc_fence_before();
+    }
+    __syncthreads();
+    tc_fence_after();
+    if (threadIdx.x == 0 && n >= 2000) {   // exact layer MMA sequence: 64 chunks x 4 k-steps x 3 products
+        const int variant = n - 2000;
+        using Cfg = GemmCfg<kFP32>;
+        const long long t0 = clock64();
+        int stage = 0, ast = 0, acc = 0;
+        const int nchunk = (variant & 16) ? 25600 : 256;
+        for (int c = 0; c < nchunk; ++c) {
+            const uint32_t d_tmem = tmem + (uint32_t)(acc * kNT);
+            const uint32_t bbase = smem_u32(smem) + stage * 0;   // one 32 KB stage: hi plane + lo plane
+            const uint32_t abase = tmem + Cfg::TMEM_A0 + ast * Cfg::A_COLS;
+            tc_fence_after();
+            if (variant & 8) {   // product-major order: consecutive MMAs never share A columns
+#pragma unroll
+                for (int p = 0; p < 3; ++p)
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks) {
+                        const uint32_t koff = ks * 32;
+                        const uint64_t b0 = umma_desc_kmajor(bbase + koff, 128);
+                        const uint64_t b1 = umma_desc_kmajor(bbase + 16384 + koff, 128);
+                        const uint32_t accum = ((c & 63) | ks | p) != 0 ? 1u : 0u;
+                        const uint32_t a_hi = abase + ks * 8, a_lo = a_hi + 32;
+                        if (p == 0) mma_tf32_ts(d_tmem, a_lo, b0, Cfg::IDESC, accum);
+                        else if (p == 1) mma_tf32_ts(d_tmem, a_hi, b1, Cfg::IDESC, 1u);
+                        else mma_tf32_ts(d_tmem, a_hi, b0, Cfg::IDESC, 1u);
+                    }
+            } else {
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+                const uint32_t koff = ks * 32;
+                const uint64_t b0 = umma_desc_kmajor(bbase + koff, 128);
+                const uint64_t b1 = umma_desc_kmajor(bbase + 16384 + koff, 128);
+                const uint32_t accum = ((c & 63) | ks) != 0 ? 1u : 0u;
+                const uint32_t a_hi = abase + ks * 8, a_lo = a_hi + 32;
+                if (variant & 1) {
+                    mma_tf32_ts(d_tmem, a_hi, b0, Cfg::IDESC, accum);
+                    mma_tf32_ts(d_tmem, a_hi, b0, Cfg::IDESC, 1u);
+                    mma_tf32_ts(d_tmem, a_hi, b0, Cfg::IDESC, 1u);
+                } else {
+                    mma_tf32_ts(d_tmem, a_lo, b0, Cfg::IDESC, accum);
+                    mma_tf32_ts(d_tmem, a_hi, b1, Cfg::IDESC, 1u);
+                    mma_tf32_ts(d_tmem, a_hi, b0, Cfg::IDESC, 1u);
+                }
+            }
+            }
+            mma_commit(&s_bar[0]);
+            if (!(variant & 4)) mma_commit(&s_bar[1]);
+            if (++ast == 4) ast = 0;
+            if ((c & 63) == 63) acc ^= (variant & 2) ? 0 : 1;
+        }
+        mma_commit(&s_bar[0]);
+        const long long t1 = clock64();
+        out[blockIdx.x * 4 + 0] = t1 - t0;
+        out[blockIdx.x * 4 + 1] = (t1 - t0) / nchunk;
+    }
+    if (n >= 2000) { __syncthreads(); tc_fence_before(); __syncthreads(); if (warp == 0) { tc_fence_after(); tmem_dealloc(tmem, 512); } return; }
+    if (threadIdx.x == 0 && n >= 1000) {   // chunk-loop variants: n = 1000 + variant
+        const int variant = n - 1000;
+        const uint64_t b = umma_desc_kmajor(smem_u32(smem), 128);
+        constexpr uint32_t idesc = umma_idesc(2u, 128, 128);
+        uint32_t ph = 0;
+        const long long t0 = clock64();
+        for (int c = 0; c < 64; ++c) {
+            if (variant & 1) tc_fence_after();
+            if (variant & 4) { while (!mbar_try_wait(&s_bar[1], 1)) {} }   // already-complete parity
+#pragma unroll
+            for (int i = 0; i < 12; ++i) mma_tf32_ts(tmem, tmem + 256 + (i & 3) * 8, b + ((i & 3) * 2), idesc, (c | i) > 0);
+            if (variant & 2) { mma_commit(&s_bar[0]); }
+        }
+        mma_commit(&s_bar[0]);
+        const long long t1 = clock64();
+        out[0] = t1 - t0;
+        out[1] = (t1 - t0) / 64;
+        out[2] = 0; out[3] = 0;
+    }
+    if (n >= 1000) { __syncthreads(); tc_fence_before(); __syncthreads(); if (warp == 0) { tc_fence_after(); tmem_dealloc(tmem, 512); } return; }
+    if (threadIdx.x == 0) {
+        const uint64_t b = umma_desc_kmajor(smem_u32(smem), 128);
+        constexpr uint32_t idesc = umma_idesc(2u, 128, 128);
+        const long long t0 = clock64();
+        for (int i = 0; i < n; ++i) mma_tf32_ts(tmem, tmem + 256, b, idesc, i > 0);
+        const long long t1 = clock64();
+        mma_commit(&s_bar[0]);
+        while (!mbar_try_wait(&s_bar[0], 0)) {}
+        const long long t2 = clock64();
+        out[0] = t1 - t0;   // issue time
+        out[1] = t2 - t0;   // issue -> completion observed
+    }
+    __syncthreads();
+    if (warp == 1) {
+        uint32_t v[16];
+        for (int i = 0; i < 16; ++i) v[i] = i;
+        const long long t0 = clock64();
+        for (int r = 0; r < 8; ++r) tmem_st16(tmem + ((uint32_t)32 << 16) + 256 + r * 16, v);
+        tmem_wait_st();
+        const long long t1 = clock64();
+        if ((threadIdx.x & 31) == 0) out[2] = t1 - t0;   // 8 x st.x16 + wait::st
+    }
+    __syncthreads();
+    if (threadIdx.x == 64) {   // wakeup latency: thread 96 arrives, thread 64 waits
+        const long long t0 = clock64();
+        while (!mbar_try_wait(&s_bar[1], 0)) {}
+        out[3] = clock64() - t0;
+    } else if (threadIdx.x == 96) {
+        const long long t0 = clock64();
+        while (clock64() - t0 < 2000) {}
+        mbar_arrive(&s_bar[1]);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) { tc_fence_after(); tmem_dealloc(tmem, 512); }
+}
+
+cudaError_t launch_debug_latency(int n, unsigned long long* out) {
+    cudaFuncSetAttribute(debug_latency_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 34 * 1024);
+    const int grid = (n >= 2000 && (n - 2000) & 32) ? 148 : 1;
+    debug_latency_kernel<<<grid, 128, 34 * 1024>>>(n, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_debug_mma_rate(int kind, int N, int iters, int nissuers, unsigned long long* out) {
+    cudaFuncSetAttribute(debug_mma_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 161 * 1024);
+    const int walk = (nissuers >> 4) & 1;
+    const int grid = (nissuers >> 8) & 255 ? (nissuers >> 8) & 255 : 1;   // number of SMs running the benchmark
+    const int threads = (nissuers >> 16) ? 384 : 128;                      // + 8 spinning warps
+    debug_mma_rate_kernel<<<grid, threads, 161 * 1024>>>(kind, N, iters, nissuers & 15, out, walk);
+    return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- host-visible launchers

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -112,6 +113,7 @@ struct RankRes {
     int32_t* slot_counts = nullptr;
     uint32_t* blk_ready = nullptr;
     unsigned long long* trace = nullptr;
+    unsigned long long* chunklog = nullptr;
     int ctas = 0;
     uint8_t* ctrl = nullptr;        // bar | heads | err | stats | sent | g0done
     float* in_buf = nullptr;
@@ -197,6 +199,7 @@ fdmoe_status alloc_rank(fdmoe_handle* h, RankRes& r, int ctas_per_rank) {
     parts.push_back({(void**)&r.tbl_w, (size_t)d.E * d.C * 4});
     parts.push_back({(void**)&r.slot_counts, (size_t)d.E * 4});
     parts.push_back({(void**)&r.trace, (size_t)ctas_per_rank * kTracePts * 8});
+    parts.push_back({(void**)&r.chunklog, (size_t)kChunkLog * 4 * 8});
     parts.push_back({(void**)&r.blk_ready, (size_t)(d.S + kGateTok - 1) / kGateTok * 4});
     parts.push_back({(void**)&r.ctrl, ctrl_bytes(d)});
     parts.push_back({(void**)&r.in_buf, (size_t)d.S * d.H * 4});
@@ -245,6 +248,7 @@ fdmoe_status build_ctx(fdmoe_handle* h) {
             c.cnt_cta = r.cnt_cta; c.tbl_tok = r.tbl_tok; c.tbl_w = r.tbl_w; c.slot_counts = r.slot_counts;
             c.blk_ready = r.blk_ready;
             c.trace = r.trace;
+            c.chunklog = getenv("FDMOE_CHUNKLOG") ? r.chunklog : nullptr;
             c.bar = reinterpret_cast<unsigned long long*>(r.ctrl + kCtrlBar);
             c.gemm_head = reinterpret_cast<uint32_t*>(r.ctrl + kCtrlGemm);
             c.comb_head = reinterpret_cast<uint32_t*>(r.ctrl + kCtrlComb);
@@ -488,6 +492,8 @@ static fdmoe_status launch_all(fdmoe_handle* h, const float* const* in_dev, floa
         p.budget_ns = (unsigned long long)budget_ms * 1000000ull;
         p.abort_flag = g.d_abort;
         p.sequential = 0;
+        const char* dbg = getenv("FDMOE_DEBUG");   // ablation switches (tools/ablate.py); unset in production
+        p.debug = dbg ? atoi(dbg) : 0;
         CK(cudaSetDevice(g.dev));
         cudaStream_t s = g.stream;
         if (streams && streams[g.members[0]]) s = static_cast<cudaStream_t>(streams[g.members[0]]);
@@ -632,7 +638,16 @@ fdmoe_status fdmoe_read_trace(fdmoe_handle* h, int32_t local_rank, uint64_t* out
     for (auto& g : h->groups) if (g.dev == r.dev) CK(cudaEventSynchronize(g.ev1));
     const int n = std::min(cap / kTracePts, r.ctas);
     CK(cudaMemcpy(out, r.trace, (size_t)n * kTracePts * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemset(r.trace, 0, (size_t)r.ctas * kTracePts * 8));
     if (n_ctas) *n_ctas = r.ctas;
+    return FDMOE_OK;
+}
+
+fdmoe_status fdmoe_read_chunklog(fdmoe_handle* h, uint64_t* out) {
+    RankRes& r = h->ranks[0];
+    CK(cudaSetDevice(r.dev));
+    for (auto& g : h->groups) if (g.dev == r.dev) CK(cudaEventSynchronize(g.ev1));
+    CK(cudaMemcpy(out, r.chunklog, (size_t)kChunkLog * 4 * 8, cudaMemcpyDeviceToHost));
     return FDMOE_OK;
 }
 
@@ -714,6 +729,35 @@ fdmoe_status fdmoe_debug_gemm(int32_t prec, int32_t K, const float* W, const flo
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(D, dD, 128 * 128 * 4, cudaMemcpyDeviceToHost));
     cudaFree(dw); cudaFree(dxh); cudaFree(dxl); cudaFree(dD); cudaFree(abort_flag);
+    return FDMOE_OK;
+}
+
+// Cycles per tcgen05.mma (M=128) issued back to back: kind 0 tf32 / 1 bf16, ts = A from TMEM.
+fdmoe_status fdmoe_debug_mma_rate(int32_t kind, int32_t nissuers, int32_t N, int32_t iters, double* cycles_per_mma) {
+    unsigned long long* d = nullptr;
+    CK(cudaMalloc(&d, 8 * 256));
+    CK(cudaMemset(d, 0, 8 * 256));
+    CK(launch_debug_mma_rate(kind, N, iters, nissuers, d));
+    CK(cudaDeviceSynchronize());
+    unsigned long long cs[256];
+    CK(cudaMemcpy(cs, d, 8 * 256, cudaMemcpyDeviceToHost));
+    unsigned long long c = 0;
+    for (int i = 0; i < 256; ++i) c = std::max(c, cs[i]);   // slowest SM
+    cudaFree(d);
+    *cycles_per_mma = (double)c / ((double)iters * (nissuers & 15));
+    return FDMOE_OK;
+}
+
+// Latency probe (cycles): [0] issue of n MMAs, [1] issue -> commit completion observed,
+// [2] 8 x tcgen05.st.x16 + wait::st, [3] mbarrier wait including a 2000-cycle delayed arrive.
+fdmoe_status fdmoe_debug_latency(int32_t n, uint64_t* out4) {
+    unsigned long long* d = nullptr;
+    CK(cudaMalloc(&d, 32 * 148));
+    CK(cudaMemset(d, 0, 32 * 148));
+    CK(launch_debug_latency(n, d));
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(out4, d, 32, cudaMemcpyDeviceToHost));
+    cudaFree(d);
     return FDMOE_OK;
 }
 

@@ -18,3 +18,6 @@ print("kernel ms", op.last_kernel_ms())
 for i, n in enumerate(names):
     print(f"{n:9s} min {t[:, i].min():9.1f}  med {np.median(t[:, i]):9.1f}  max {t[:, i].max():9.1f} us")
 print("ffn tiles per CTA: min", int(t[:, 7].min()), "max", int(t[:, 7].max()), "sum", int(t[:, 7].sum()))
+ffn_cyc = (t[:, 4] - t[:, 3]).mean() * 1e3 * 1.965   # ns -> cycles at max clock (approx)
+for i, n in enumerate(["mma<-tokens", "mma<-weights", "mma<-acc", "conv<-wTMA", "conv<-tmemA", "prod<-wslot", "prod<-xslot", "epi<-acc"]):
+    print(f"wait {n:14s} mean {t[:, 8 + i].mean() / 1e3:9.1f} kcyc  ({100 * t[:, 8 + i].mean() / ffn_cyc:5.1f}% of FFN phase)")
