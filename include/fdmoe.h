@@ -79,6 +79,11 @@ typedef struct fdmoe_options {
     int32_t processors;         /* reference processor threads per device (ignored) */
     int32_t sequential;         /* ScheduleMode::sequential (bulk-synchronous baseline) */
     int64_t deadlock_budget_ms; /* in-kernel watchdog budget (runtime.hpp:90, default 5000) */
+    int32_t exact_gate;         /* 1: reference-exact gate logits for every token (G_phi and
+                                 * combine weights bit-identical to the reference); 0 (default):
+                                 * certified gate — FFMA logits, routing (assignment, slots, drops)
+                                 * proven identical per token, exact recompute where unproven */
+    int32_t reserved;
 } fdmoe_options;
 
 /* Per-rank routing surface (GateOutput, gate.hpp:24-37). All host pointers, nullable.
@@ -106,6 +111,9 @@ typedef struct fdmoe_stats {
     int64_t gemm0, gemm1, combine, enqueued, executed;
     int64_t bound_initial, bound_final, scheduled_final, launches;
     double kernel_ms;     /* device time of the layer launch on this rank (CUDA events) */
+    int64_t gate_exact_tokens; /* tokens whose logits were recomputed exactly for all experts
+                                * (all S with exact_gate; ties / near-ties otherwise) */
+    int64_t gate_pair_tokens;  /* tokens the certified gate decided from exact candidate logits */
 } fdmoe_stats;
 
 typedef struct fdmoe_handle fdmoe_handle;
@@ -167,7 +175,7 @@ fdmoe_status fdmoe_forward(fdmoe_handle* h, const float* const* in_shards, float
 /* Asynchronous device-pointer variant: enqueue on streams[i] (cudaStream_t as void*,
  * one per local rank; NULL = the handle's own stream). Pair with fdmoe_sync. */
 fdmoe_status fdmoe_forward_async(fdmoe_handle* h, const float* const* in_dev, float* const* out_dev,
-                                 void* const* streams);
+                                 void* const* streams, const fdmoe_options* opts);
 /* Wait for the last forward, check the device watchdog/error word. */
 fdmoe_status fdmoe_sync(fdmoe_handle* h);
 

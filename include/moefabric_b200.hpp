@@ -207,6 +207,7 @@ struct ForwardOptions {
     std::int64_t deadlock_budget_ms = 5000;
     std::uint64_t seed = 0;
     std::vector<std::int32_t> device_ids;   // B200 addition: CUDA device per rank (default all 0)
+    bool exact_gate = false;                // B200 addition: reference-exact gate logits (fdmoe.h)
 };
 struct TaskStats {
     std::int64_t gemm0 = 0, gemm1 = 0, combine = 0, enqueued = 0, executed = 0;
@@ -291,6 +292,7 @@ inline ForwardResult forward(const MoeConfig& cfg, const std::vector<TokenMatrix
     o.processors = opts.processors;
     o.sequential = opts.mode == ScheduleMode::sequential ? 1 : 0;
     o.deadlock_budget_ms = opts.deadlock_budget_ms;
+    o.exact_gate = opts.exact_gate ? 1 : 0;
     detail::check(fdmoe_forward(h, in.data(), out.data(), FDMOE_HOST, &o, ro.data(), st.data()));
 
     double kernel_ms = 0.0;

@@ -90,7 +90,8 @@ class _Cfg(C.Structure):
 
 
 class _Opts(C.Structure):
-    _fields_ = [("processors", C.c_int32), ("sequential", C.c_int32), ("deadlock_budget_ms", C.c_int64)]
+    _fields_ = [("processors", C.c_int32), ("sequential", C.c_int32), ("deadlock_budget_ms", C.c_int64),
+                ("exact_gate", C.c_int32), ("reserved", C.c_int32)]
 
 
 class _Routing(C.Structure):
@@ -102,7 +103,8 @@ class _Routing(C.Structure):
 class _Stats(C.Structure):
     _fields_ = [("gemm0", C.c_int64), ("gemm1", C.c_int64), ("combine", C.c_int64), ("enqueued", C.c_int64),
                 ("executed", C.c_int64), ("bound_initial", C.c_int64), ("bound_final", C.c_int64),
-                ("scheduled_final", C.c_int64), ("launches", C.c_int64), ("kernel_ms", C.c_double)]
+                ("scheduled_final", C.c_int64), ("launches", C.c_int64), ("kernel_ms", C.c_double),
+                ("gate_exact_tokens", C.c_int64), ("gate_pair_tokens", C.c_int64)]
 
 
 class _Info(C.Structure):
@@ -158,7 +160,7 @@ def lib():
         "fdmoe_import_peers": (i32, [vp, vp, i32]),
         "fdmoe_set_weights": (i32, [vp, f32p, f32p, f32p, f32p, f32p, i32]),
         "fdmoe_forward": (i32, [vp, vp, vp, i32, C.POINTER(_Opts), vp, vp]),
-        "fdmoe_forward_async": (i32, [vp, vp, vp, vp]),
+        "fdmoe_forward_async": (i32, [vp, vp, vp, vp, vp]),
         "fdmoe_sync": (i32, [vp]),
         "fdmoe_get_info": (i32, [vp, C.POINTER(_Info)]),
         "fdmoe_last_kernel_ms": (i32, [vp, vp]),
@@ -224,6 +226,13 @@ class ForwardOptions:
     sequential: bool = False
     deadlock_budget_ms: int = 5000
     seed: int = 0
+    # B200 addition: True = reference-exact gate logits for every token (G_phi and combine weights
+    # bit-identical); False = certified gate (routing proven identical per token)
+    exact_gate: bool = False
+
+    def to_c(self):
+        return _Opts(self.processors, 1 if self.sequential else 0, self.deadlock_budget_ms,
+                     1 if self.exact_gate else 0, 0)
 
 
 @dataclasses.dataclass
@@ -271,6 +280,8 @@ class TaskStats:
     scheduled_final: int = 0
     launches: int = 0
     kernel_ms: float = 0.0
+    gate_exact_tokens: int = 0
+    gate_pair_tokens: int = 0
 
     def total(self) -> int:
         return self.gemm0 + self.gemm1 + self.combine
@@ -459,7 +470,7 @@ class Operator:
         in_p = (C.c_void_p * n)(*[a.ctypes.data for a in ins])
         out_p = (C.c_void_p * n)(*[a.ctypes.data for a in outs])
         o = opts or ForwardOptions()
-        copts = _Opts(o.processors, 1 if o.sequential else 0, o.deadlock_budget_ms)
+        copts = o.to_c()
         cap = expert_capacity(cfg)
         rt = (_Routing * n)()
         keep = []
@@ -496,13 +507,15 @@ class Operator:
             b = np.zeros(cfg.devices * cfg.devices, np.uint64)
         return ForwardResult(outs, gates, manifests, [], b, padded_baseline_bytes(cfg), stats_l, t1 - t0)
 
-    def forward_device(self, in_ptrs: Sequence[int], out_ptrs: Sequence[int], streams: Optional[Sequence[int]] = None):
+    def forward_device(self, in_ptrs: Sequence[int], out_ptrs: Sequence[int], streams: Optional[Sequence[int]] = None,
+                       opts: Optional[ForwardOptions] = None):
         """Asynchronous forward on device pointers (one kernel launch per device)."""
         n = self.n_local
         ip = (C.c_void_p * n)(*in_ptrs)
         op = (C.c_void_p * n)(*out_ptrs)
         sp = (C.c_void_p * n)(*(streams or [0] * n))
-        _check(lib().fdmoe_forward_async(self._h, ip, op, sp))
+        copts = (opts or ForwardOptions()).to_c()
+        _check(lib().fdmoe_forward_async(self._h, ip, op, sp, C.byref(copts)))
 
     def sync(self):
         _check(lib().fdmoe_sync(self._h))

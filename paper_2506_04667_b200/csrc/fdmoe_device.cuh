@@ -63,6 +63,8 @@ struct alignas(64) RankCtx {
     const float* b1;           // [E_local][D]
     const float* b2;           // [E_local][H]
     const float* wg;           // [H][E_total]
+    const float* wg_norm;      // [E_total] |Wg[:, e]|_2 rounded up (certified gate)
+    const float* wgT;          // [E_total][H] Wg transposed (certified gate's exact pair pass)
     float* g_phi;              // [S][E_total]
     int32_t* pick_e;           // [S][k]
     int32_t* pick_slot;        // [S][k]  (-1 = capacity-dropped)
@@ -99,6 +101,9 @@ struct LaunchParams {
     uint32_t* abort_flag;      // per launch-group abort word
     int sequential;            // bulk-synchronous schedule (grid barrier after each phase)
     int debug;                 // ablation bits (FDMOE_DEBUG env; 0 in production): see kDbg*
+    int exact_gate;            // 1: reference-exact logits for every token (bit-exact G_phi, weights)
+    float gate_u;              // certified gate: u' = 2^-24 * 1.001
+    float gate_k1;             // certified gate: 66 + 2 H gamma_{H+1}
 };
 enum DebugBits : int {
     kDbgNoConvert = 1,    // converter warps skip the split + tcgen05.st (MMA reads stale TMEM)
@@ -106,6 +111,10 @@ enum DebugBits : int {
     kDbgNoEpiStore = 4,   // epilogue skips global stores
     kDbgNoXTma = 8,       // producer skips the token TMA (barrier completes without data)
     kDbgNoWTma = 16,      // producer skips the weight TMA
+    kDbgGateNoNorm = 32,  // certified gate skips the |a|^2 accumulation (bounds wrong: timing only)
+    kDbgGateNoFlush = 64, // certified gate skips the exact pass (routing wrong: timing only)
+    kDbgGateNoLoad = 128, // gate skips its cp.async loads (timing only)
+    kDbgGateNoMath = 256, // gate skips its dot-product loop (timing only)
 };
 
 // Error codes written to RankCtx::err[0] (mirrors the reference's exceptions).

@@ -180,19 +180,58 @@ __device__ bool rank_barrier(const LaunchParams& P, const RankCtx& R, unsigned l
     return s_ok != 0;
 }
 
-// ================================================================ phase 1: exact gate
+// ================================================================ phase 1: gate
 // Each CTA owns a contiguous, balanced token range (its gate blocks [b0, b1)), processed in
-// sub-tiles of <= 64 tokens. Logits are FP32 sequential dot products over x ascending with a
-// separately rounded multiply and add (gate.hpp:77-81 as compiled with -ffp-contract=off);
-// each thread owns 4 tokens x 8 experts and streams K through a 3-stage cp.async ring:
-//   sA[stage][64][36]  token rows (32 K values + 4 pad floats: conflict-free column reads)
-//   sW[stage][32][Ep]  Wg rows
-// then one warp per token does max / glibc-exp / sequential sum / divide / top-k.
-constexpr int kGateSub = 64;
+// sub-tiles of <= gate_sub(Ep) tokens (120 at E <= 128); K streams through a 3-stage cp.async ring
+//   sA[stage][sub][36]  token rows (32 K values + 4 pad floats: conflict-free LDS.128)
+//   sW[stage][32][Ep]   Wg rows
+// and every thread owns a 5-token x 8-expert tile of logits (one pass, all 384 threads busy).
+//
+// Two ways to get the reference's routing (gate.hpp:57-106):
+//  * exact (ForwardOptions::exact_gate): logits as the reference computes them — FP32 sequential
+//    dot products over x ascending, multiply and add rounded separately (gate.hpp:77-81 built
+//    -ffp-contract=off) — then max / glibc expf / sequential sum / divide / top-k: G_phi, weights
+//    and picks bit-identical.
+//  * certified (default): one FFMA per MAC, and a rigorous per-token bound on |z~_e - z_ref_e|:
+//    both chains are sequential sums, whose error is <= u * sum_i |partial_i| (Higham, Accuracy and
+//    Stability, eq. 4.3). Partials inside a 32-term chunk are bounded by the chunk-start partial plus
+//    the chunk's |products|, so with Sab = sum over chunk ends of |z~ partial| (one FADD per chunk)
+//        beta_e = u' * (64 * Sab + k1 * |a| |w_e|),   k1 = 66 + 2H gamma_{H+1}
+//    (u' = 2^-24 * 1.001; the k1 term covers product rounding and the chains' mutual distance).
+//    Typical beta ~ 3e-4 for unit-scale logits at H = 2048 — 40x tighter than gamma_H |a||w|.
+//    Per token: with intervals [z~ - beta, z~ + beta], experts whose upper bound is below the k-th
+//    largest lower bound (less a margin covering expf/divide rounding) are provably not picked. If
+//    exactly k candidates remain and their order is separated, the reference's picks, order, slots
+//    and drops are proven identical. Otherwise the candidates (<= 8) get their EXACT reference
+//    logits (a separately-rounded chain per (token, expert) pair, staged through smem), and the
+//    picks are decided on exact values when their gaps exceed the rounding of expf/divide; tokens
+//    with ties or near-ties fall back to the full exact path. G_phi and combine weights of
+//    non-full-exact tokens derive from z~ (relative error ~1e-6: tolerance, not bits).
+constexpr int kGateTT = 5;                  // tokens per thread tile
+constexpr int kGateTE = 8;                  // experts per thread tile
+constexpr int kGateSubMax = 120;
 constexpr int kGateStages = 3;
 constexpr int kGateApitch = kGateKC + 4;
-constexpr int kGateSmemBytes = (kGateSub * kMaxExperts + kGateStages * kGateSub * kGateApitch +
-                                kGateStages * kGateKC * kMaxExperts + kMaxExperts) * 4;
+constexpr int kGateMaxCand = 8;             // candidate experts per token for the pair pass
+constexpr int kGatePairCap = 256;           // (token, expert) pairs per sub-tile
+constexpr int kGatePairBatch = 16;          // pairs per smem-staged batch (one thread each)
+constexpr int kGatePairX = 256;             // x-chunk of the pair pass
+constexpr int kGatePairPitch = 2 * kGatePairX + 4;
+__host__ __device__ constexpr int gate_sub(int Ep) {
+    return kGateTT * (kThreads / (Ep / kGateTE)) < kGateSubMax ? kGateTT * (kThreads / (Ep / kGateTE)) : kGateSubMax;
+}
+__host__ __device__ constexpr int gate_region_floats(int Ep) {
+    return gate_sub(Ep) * Ep + kGateStages * gate_sub(Ep) * kGateApitch + kGateStages * kGateKC * Ep;
+}
+constexpr int gate_region_max() {
+    int m = 0;
+    for (int Ep = 8; Ep <= kMaxExperts; Ep += 8) m = gate_region_floats(Ep) > m ? gate_region_floats(Ep) : m;
+    return m;
+}
+constexpr int kGateRegionFloats = gate_region_max();
+static_assert(kGateSubMax * 128 + 2 * kGatePairBatch * kGatePairPitch <= kGateRegionFloats, "pair buffer fits");
+constexpr int kGateSmemBytes = ((kGateRegionFloats * 4 + 15) & ~15) + kMaxExperts * 4 /*sCnt*/ + kGateSubMax * (4 + 8 + 4 + 4 + 4) +
+                               kGatePairCap * 12 + 16;
 static_assert(kGateTok <= 32, "slot assignment maps one gate block onto one warp");
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
@@ -213,47 +252,64 @@ __device__ __forceinline__ void gate_token_range(const LaunchParams& P, int cta,
     tokB = min(P.S, b1 * kGateTok);
 }
 
-__device__ void gate_phase(const LaunchParams& P, const RankCtx& R, const float* __restrict__ A, int cta,
-                           uint8_t* smem) {
-    const int E = P.E, H = P.H, K = P.k;
+struct GateSmem {
+    float* sL;       // [sub][Ep] logits -> exps
+    float* sA;       // [stages][sub][36]
+    float* sW;       // [stages][32][Ep]
+    float* sPair;    // [2][16][kGatePairPitch] pair-pass staging (aliases sA/sW, never sL)
+    int* sCnt;       // [Ep] CTA-level pick counts
+    float* sSab;     // [sub] max over experts of sum |chunk-end partial|
+    double* sNa;     // [sub] |a|^2
+    int* sTP0;       // [sub] first pair of token t
+    int* sTNC;       // [sub] candidate count of token t (0: routed or full-exact)
+    int* sFull;      // [sub] tokens for the full exact pass
+    int* sPT;        // [cap] pair token
+    int* sPE;        // [cap] pair expert
+    float* sPZ;      // [cap] pair exact logit
+    int sub;
+};
+
+// Expert column of a thread's float4 group j (j % 4 == 0): group q = j / 4 of thread eg covers
+// experts q * Ep / (TE / 4) + 4 eg + [0, 4) — a warp's float4 loads are contiguous (no bank conflicts).
+__device__ __forceinline__ int gate_col(int eg, int j, int Ep, int TE) { return (j >> 2) * (Ep / (TE >> 2)) + 4 * eg; }
+
+// two independent round-to-nearest FMAs in one FFMA2: (d0, d1) += a * (b0, b1)
+__device__ __forceinline__ void ffma2_bcast(float& d0, float& d1, float a, float b0, float b1) {
+    unsigned long long d, b;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(d0), "f"(d1));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(b) : "f"(b0), "f"(b1));
+    asm("{\n\t.reg .b64 aa;\n\tmov.b64 aa, {%2, %2};\n\tfma.rn.f32x2 %0, aa, %1, %0;\n\t}" : "+l"(d) : "l"(b), "f"(a));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(d));
+}
+
+// Logits of `ts` tokens (token t = rows ? rows[t] : tok0 + t) into sL[t][e]. Thread tile TT x TE.
+// FAST: fma chain + chunk-end |partial| sums into sSab + |a|^2 into sNa; else the reference chain.
+template <bool FAST, int TT, int TE>
+__device__ void gate_logits(const LaunchParams& P, const RankCtx& R, const float* __restrict__ A, int tok0,
+                            const int* rows, int ts, const GateSmem& g) {
+    const int E = P.E, H = P.H;
     const int Ep = (E + 7) & ~7;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    float* sL = reinterpret_cast<float*>(smem);                                   // [64][Ep]
-    float* sA = sL + kGateSub * Ep;                                              // [stages][64][36]
-    float* sW = sA + kGateStages * kGateSub * kGateApitch;                       // [stages][32][Ep]
-    int* sCnt = reinterpret_cast<int*>(sW + kGateStages * kGateKC * Ep);        // [Ep]
-    for (int e = tid; e < Ep; e += kThreads) sCnt[e] = 0;
+    const int tid = threadIdx.x;
     const bool w_vec = (E & 3) == 0;
-
-    int tokA, tokB, b0, b1;
-    gate_token_range(P, cta, tokA, tokB, b0, b1);
-    const int ntok = tokB - tokA;
-    const int nsub = (ntok + kGateSub - 1) / kGateSub;
-    const int n_eg = Ep / 8;
+    const int n_eg = Ep / TE;
+    const int n_tg = (ts + TT - 1) / TT;
+    const int n_items = n_tg * n_eg;
     const int nk = H / kGateKC;   // envelope: H % 32 == 0
-
-    for (int si = 0; si < nsub; ++si) {
-        // balanced sub-tiles, multiples of 4 tokens
-        const int s0 = (int)((long long)ntok * si / nsub) & ~3;
-        const int s1 = si + 1 == nsub ? ntok : ((int)((long long)ntok * (si + 1) / nsub) & ~3);
-        const int ts = s1 - s0;
-        const int n_tg = (ts + 3) / 4;
-        const int n_items = n_tg * n_eg;
-        const float* Abase = A + (size_t)(tokA + s0) * H;
-
+    for (int base = 0; base < n_items; base += kThreads) {   // item rounds (re-stream K per round)
         auto load_stage = [&](int st, int kb) {
-            float* a = sA + st * kGateSub * kGateApitch;
-            float* w = sW + st * kGateKC * Ep;
+            if (P.debug & kDbgGateNoLoad) { cp_async_commit(); return; }
+            float* a = g.sA + st * g.sub * kGateApitch;
+            float* w = g.sW + st * kGateKC * Ep;
             const int k0 = kb * kGateKC;
-            for (int i = tid; i < kGateSub * 8; i += kThreads) {
+            for (int i = tid; i < ts * 8; i += kThreads) {
                 const int t = i >> 3, c = i & 7;
-                const bool ok = t < ts;
-                cp_async16(a + t * kGateApitch + c * 4, Abase + (size_t)(ok ? t : 0) * H + k0 + c * 4, ok);
+                const int tok = rows ? rows[t] : tok0 + t;
+                cp_async16(a + t * kGateApitch + c * 4, A + (size_t)tok * H + k0 + c * 4, true);
             }
             if (w_vec) {
-                const int cpr = Ep / 4;
+                const int cpr = Ep >> 2;
                 for (int i = tid; i < kGateKC * cpr; i += kThreads) {
-                    const int kk = i / cpr, c = i % cpr;
+                    const int kk = i / cpr, c = i - kk * cpr;
                     const bool ok = c * 4 < E;
                     cp_async16(w + kk * Ep + c * 4, R.wg + (size_t)(k0 + kk) * E + (ok ? c * 4 : 0), ok);
                 }
@@ -265,16 +321,19 @@ __device__ void gate_phase(const LaunchParams& P, const RankCtx& R, const float*
             }
             cp_async_commit();
         };
+        float acc[TT][TE], sab[TT];   // sab: sum over chunk ends of max_j |partial| (bounds every j's sum)
+#pragma unroll
+        for (int i = 0; i < TT; ++i) {
+            sab[i] = 0.0f;
+#pragma unroll
+            for (int j = 0; j < TE; ++j) acc[i][j] = 0.0f;
+        }
+        double ss = 0.0;
+        const int item = base + tid;
+        const int tg = item / n_eg, eg = item % n_eg;
+        const bool active = item < n_items;
 
-        float acc[2][4][8];
-#pragma unroll
-        for (int it = 0; it < 2; ++it)
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 8; ++j) acc[it][i][j] = 0.0f;
-
-        __syncthreads();   // previous sub-tile's readers of sA/sW/sL are done
+        __syncthreads();   // previous users of sA/sW/sL are done
         for (int st = 0; st < kGateStages - 1; ++st)
             if (st < nk) load_stage(st, st); else cp_async_commit();
         for (int kb = 0; kb < nk; ++kb) {
@@ -283,107 +342,449 @@ __device__ void gate_phase(const LaunchParams& P, const RankCtx& R, const float*
             else cp_async_commit();
             cp_async_wait<kGateStages - 1>();
             __syncthreads();
-            const float* a = sA + st * kGateSub * kGateApitch;
-            const float* w = sW + st * kGateKC * Ep;
+            const float* a = g.sA + st * g.sub * kGateApitch;
+            const float* w = g.sW + st * kGateKC * Ep;
+            if (FAST && tid < ts && !(P.debug & kDbgGateNoNorm)) {   // |a|^2: 32-term float chunks, double sum
+                const float* ar = a + tid * kGateApitch;
+                float cs = 0.0f;
 #pragma unroll
-            for (int it = 0; it < 2; ++it) {
-                const int item = tid + it * kThreads;
-                if (item < n_items) {
-                    const int tg = item / n_eg, eg = item % n_eg;
-                    const float* ar = a + (4 * tg) * kGateApitch;
-                    const float* wr = w + 8 * eg;
+                for (int kk = 0; kk < kGateKC; ++kk) cs = __fmaf_rn(ar[kk], ar[kk], cs);
+                ss += (double)cs;
+            }
+            if (active && !(P.debug & kDbgGateNoMath)) {
+                const float* ar = a + (TT * tg) * kGateApitch;
 #pragma unroll 8
-                    for (int kk = 0; kk < kGateKC; ++kk) {
-                        const float a0 = ar[kk], a1 = ar[kGateApitch + kk], a2 = ar[2 * kGateApitch + kk],
-                                    a3 = ar[3 * kGateApitch + kk];
-                        const float4 w0 = *reinterpret_cast<const float4*>(wr + kk * Ep);
-                        const float4 w1 = *reinterpret_cast<const float4*>(wr + kk * Ep + 4);
-                        const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-                        const float av[4] = {a0, a1, a2, a3};
+                for (int kk = 0; kk < kGateKC; ++kk) {
+                    float av[TT], wv[TE];
 #pragma unroll
-                        for (int i = 0; i < 4; ++i)
+                    for (int i = 0; i < TT; ++i) av[i] = ar[i * kGateApitch + kk];
 #pragma unroll
-                            for (int j = 0; j < 8; ++j)
-                                acc[it][i][j] = __fadd_rn(acc[it][i][j], __fmul_rn(av[i], wv[j]));
+                    for (int j = 0; j < TE; j += 4) {   // float4 groups spread Ep/(TE/4) apart: conflict-free
+                        const float4 w4 = *reinterpret_cast<const float4*>(w + kk * Ep + gate_col(eg, j, Ep, TE));
+                        wv[j] = w4.x; wv[j + 1] = w4.y; wv[j + 2] = w4.z; wv[j + 3] = w4.w;
+                    }
+#pragma unroll
+                    for (int i = 0; i < TT; ++i)
+#pragma unroll
+                        for (int j = 0; j < TE; j += 2) {
+                            if (FAST) {
+                                ffma2_bcast(acc[i][j], acc[i][j + 1], av[i], wv[j], wv[j + 1]);
+                            } else {
+                                acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(av[i], wv[j]));
+                                acc[i][j + 1] = __fadd_rn(acc[i][j + 1], __fmul_rn(av[i], wv[j + 1]));
+                            }
+                        }
+                }
+                if (FAST) {
+#pragma unroll
+                    for (int i = 0; i < TT; ++i) {
+                        float m = 0.0f;
+#pragma unroll
+                        for (int j = 0; j < TE; ++j) m = fmaxf(m, fabsf(acc[i][j]));
+                        sab[i] += m;
                     }
                 }
             }
             __syncthreads();   // stage st may be refilled next iteration
         }
         cp_async_wait<0>();
+        if (active) {
 #pragma unroll
-        for (int it = 0; it < 2; ++it) {
-            const int item = tid + it * kThreads;
-            if (item < n_items) {
-                const int tg = item / n_eg, eg = item % n_eg;
+            for (int i = 0; i < TT; ++i) {
+                if (TT * tg + i >= ts) continue;
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) sL[(4 * tg + i) * Ep + 8 * eg + j] = acc[it][i][j];
+                for (int j = 0; j < TE; ++j) g.sL[(TT * tg + i) * Ep + gate_col(eg, j & ~3, Ep, TE) + (j & 3)] = acc[i][j];
+                // non-negative floats order like their bit patterns; rounding of the running sum
+                // is covered by u' (1.001 u)
+                if (FAST) atomicMax(reinterpret_cast<int*>(g.sSab) + TT * tg + i, __float_as_int(sab[i]));
             }
         }
-        __syncthreads();
-
-        // softmax + top-k: one warp per token
-        for (int t = warp; t < ts; t += kThreads / 32) {
-            const int tok = tokA + s0 + t;
-            float* row = sL + t * Ep;
-            // max is exact and order-free (x - max only feeds expf; +-0 ties give equal results)
-            float mx = row[0];
-            for (int e = lane; e < E; e += 32) mx = fmaxf(mx, row[e]);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-            for (int e = lane; e < E; e += 32) row[e] = expf_glibc(__fsub_rn(row[e], mx));
-            __syncwarp();
-            float sum = 0.0f;
-            if (lane == 0)
-                for (int e = 0; e < E; ++e) sum = __fadd_rn(sum, row[e]);   // ascending e (gate.hpp:85-88)
-            sum = __shfl_sync(0xffffffffu, sum, 0);
-            for (int e = lane; e < E; e += 32) {
-                const float p = __fdiv_rn(row[e], sum);
-                row[e] = p;
-                R.g_phi[(size_t)tok * E + e] = p;
-            }
-            __syncwarp();
-            // top-k by repeated argmax on p; ties -> lower expert index (gate.hpp:41-51)
-            uint32_t taken = 0;   // bit jj: expert lane + 32*jj taken
-            float denom = 0.0f;
-            float pv[8];
-            int pe[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                if (j >= K) break;
-                float bv = -1.0f;
-                int bi = 0x7fffffff;
-                for (int e = lane, jj = 0; e < E; e += 32, ++jj) {
-                    if (taken & (1u << jj)) continue;
-                    const float v = row[e];
-                    if (v > bv || (v == bv && e < bi)) { bv = v; bi = e; }
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-                    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-                    if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-                }
-                if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
-                pe[j] = bi;
-                pv[j] = bv;
-                denom = __fadd_rn(denom, bv);   // pick order (gate.hpp:92)
-            }
-            if (lane == 0) {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    if (j >= K) break;
-                    R.pick_e[(size_t)tok * K + j] = pe[j];
-                    R.pick_w[(size_t)tok * K + j] = denom > 0.0f ? __fdiv_rn(pv[j], denom) : 0.0f;
-                    atomicAdd(&sCnt[pe[j]], 1);
-                }
-            }
-        }
+        if (FAST && tid < ts) g.sNa[tid] = ss;
     }
     __syncthreads();
-    for (int e = tid; e < E; e += kThreads) R.cnt_cta[(size_t)cta * E + e] = sCnt[e];
+}
+
+// warp argmax with lower-index tie-break
+__device__ __forceinline__ void warp_argmax(float& v, int& i) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, i, o);
+        if (ov > v || (ov == v && oi < i)) { v = ov; i = oi; }
+    }
+}
+
+// Routing outputs of one token from (approximate) logits in `row` with max `mx` and picks pe[0..K)
+// (one warp): G_phi and weights derive from row; expert ids are already decided.
+__device__ __forceinline__ void write_routing_from_row(const LaunchParams& P, const RankCtx& R, float* row, float mx,
+                                                       int tok, const int (&pe)[8], int* sCnt) {
+    const int E = P.E, K = P.k, lane = threadIdx.x & 31;
+    float part = 0.0f;
+    for (int e = lane; e < E; e += 32) {
+        const float x = expf_glibc(__fsub_rn(row[e], mx));
+        row[e] = x;
+        part += x;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    const float inv = 1.0f / part;
+    __syncwarp();
+    for (int e = lane; e < E; e += 32) R.g_phi[(size_t)tok * E + e] = row[e] * inv;
+    if (lane == 0) {
+        float denom = 0.0f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (j >= K) break;
+            denom += row[pe[j]] * inv;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (j >= K) break;
+            R.pick_e[(size_t)tok * K + j] = pe[j];
+            R.pick_w[(size_t)tok * K + j] = denom > 0.0f ? row[pe[j]] * inv / denom : 0.0f;
+            atomicAdd(&sCnt[pe[j]], 1);
+        }
+    }
+    __syncwarp();
+}
+
+// Exact routing of one token from its exact logits in `row` (one warp): gate.hpp:82-103.
+__device__ void route_exact(const LaunchParams& P, const RankCtx& R, float* row, int tok, int* sCnt) {
+    const int E = P.E, K = P.k, lane = threadIdx.x & 31;
+    // max is exact and order-free (x - max only feeds expf; +-0 ties give equal results)
+    float mx = row[0];
+    for (int e = lane; e < E; e += 32) mx = fmaxf(mx, row[e]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    for (int e = lane; e < E; e += 32) row[e] = expf_glibc(__fsub_rn(row[e], mx));
+    __syncwarp();
+    float sum = 0.0f;
+    if (lane == 0)
+        for (int e = 0; e < E; ++e) sum = __fadd_rn(sum, row[e]);   // ascending e (gate.hpp:85-88)
+    sum = __shfl_sync(0xffffffffu, sum, 0);
+    for (int e = lane; e < E; e += 32) {
+        const float p = __fdiv_rn(row[e], sum);
+        row[e] = p;
+        R.g_phi[(size_t)tok * E + e] = p;
+    }
+    __syncwarp();
+    // top-k by repeated argmax on p; ties -> lower expert index (gate.hpp:41-51)
+    uint32_t taken = 0;   // bit jj: expert lane + 32*jj taken
+    float denom = 0.0f;
+    float pv[8];
+    int pe[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        if (j >= K) break;
+        float bv = -1.0f;
+        int bi = 0x7fffffff;
+        for (int e = lane, jj = 0; e < E; e += 32, ++jj) {
+            if (taken & (1u << jj)) continue;
+            const float v = row[e];
+            if (v > bv || (v == bv && e < bi)) { bv = v; bi = e; }
+        }
+        warp_argmax(bv, bi);
+        if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
+        pe[j] = bi;
+        pv[j] = bv;
+        denom = __fadd_rn(denom, bv);   // pick order (gate.hpp:92)
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (j >= K) break;
+            R.pick_e[(size_t)tok * K + j] = pe[j];
+            R.pick_w[(size_t)tok * K + j] = denom > 0.0f ? __fdiv_rn(pv[j], denom) : 0.0f;
+            atomicAdd(&sCnt[pe[j]], 1);
+        }
+    }
+    __syncwarp();
+}
+
+// Margin between two logits x > y (m: the token's max logit) that keeps the reference's
+// probabilities strictly ordered: with d = fl(z - m) (error <= u|z - m|), glibc expf (< 1 ulp) and
+// the division (0.5 ulp), p_x > p_y holds once x - y > 2^-21.4 + u (|x - m| + |y - m|); we use
+// 2^-19 + 2^-21 (|x - m| + |y - m|), plus 2^-22 (|x| + |y|) for the float rounding of the bound
+// arithmetic (z~ +- beta) that produced x and y.
+__device__ __forceinline__ float gate_margin(float x, float y, float m) {
+    return 1.9073486e-6f + 4.7683716e-7f * (fabsf(x - m) + fabsf(y - m)) + 2.3841858e-7f * (fabsf(x) + fabsf(y));
+}
+
+// Certified routing of token t (local index) from FFMA logits in `row` (one warp).
+// Returns 1: routed; 0: candidates appended to the pair list; 2: needs the full exact pass.
+__device__ int route_certified(const LaunchParams& P, const RankCtx& R, float* row, int tok, int t,
+                               const GateSmem& g, int* s_np) {
+    constexpr int J = kMaxExperts / 32;
+    const int E = P.E, K = P.k, lane = threadIdx.x & 31;
+    const float na = __double2float_ru(sqrt(g.sNa[t] * (1.0 + 1e-5)));
+    const float c_s = P.gate_u * 64.0f * g.sSab[t];
+    const float c_w = P.gate_u * P.gate_k1 * na;
+    float z[J], bt[J];
+    bool bad = false;
+#pragma unroll
+    for (int jj = 0; jj < J; ++jj) {
+        const int e = lane + 32 * jj;
+        if (e < E) {
+            z[jj] = row[e];
+            bt[jj] = c_s + c_w * __ldg(R.wg_norm + e) + 1e-30f;
+            bad |= !(fabsf(z[jj]) < 1e30f) || !(bt[jj] < 1e30f);
+        } else {
+            z[jj] = -INFINITY;
+            bt[jj] = 0.0f;
+        }
+    }
+    if (__any_sync(0xffffffffu, bad)) return 2;   // NaN / inf / overflow: the exact path decides
+    // top-1 by z~ (reference max ~ z0) and the k-th largest lower bound
+    float z0 = -INFINITY;
+    {
+        int i0 = 0x7fffffff;
+#pragma unroll
+        for (int jj = 0; jj < J; ++jj)
+            if (z[jj] > z0) { z0 = z[jj]; i0 = lane + 32 * jj; }
+        warp_argmax(z0, i0);
+    }
+    float Lk = 0.0f;
+    {
+        uint32_t taken = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (j >= K) break;
+            float bv = -INFINITY;
+            int bi = 0x7fffffff;
+#pragma unroll
+            for (int jj = 0; jj < J; ++jj) {
+                const int e = lane + 32 * jj;
+                if (e >= E || (taken & (1u << jj))) continue;
+                const float lb = z[jj] - bt[jj];
+                if (lb > bv) { bv = lb; bi = e; }
+            }
+            warp_argmax(bv, bi);
+            if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
+            Lk = bv;
+        }
+    }
+    // candidates: experts whose upper bound reaches the k-th largest lower bound
+    uint32_t cmask = 0;
+    int n_c = 0;
+#pragma unroll
+    for (int jj = 0; jj < J; ++jj) {
+        const int e = lane + 32 * jj;
+        const float ub = z[jj] + bt[jj];
+        const bool c = e < E && ub >= Lk - gate_margin(ub, Lk, z0);
+        if (c) cmask |= 1u << jj;
+        n_c += __popc(__ballot_sync(0xffffffffu, c));
+    }
+    if (n_c > kGateMaxCand) return 2;
+    if (n_c == K) {
+        // the set is certain; the order is certain if consecutive z~-sorted picks are separated
+        int pe[8];
+        uint32_t taken = 0;
+        float prev_lb = 0.0f;
+        bool ok = true;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (j >= K) break;
+            float bv = -INFINITY, bb = 0.0f;
+            int bi = 0x7fffffff;
+#pragma unroll
+            for (int jj = 0; jj < J; ++jj) {
+                if (!(cmask & (1u << jj)) || (taken & (1u << jj))) continue;
+                if (z[jj] > bv) { bv = z[jj]; bi = lane + 32 * jj; bb = bt[jj]; }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                const float ob = __shfl_xor_sync(0xffffffffu, bb, o);
+                if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; bb = ob; }
+            }
+            if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
+            pe[j] = bi;
+            if (j > 0) ok &= prev_lb > bv + bb + gate_margin(prev_lb, bv + bb, z0);
+            prev_lb = bv - bb;
+        }
+        // picks far below the max could underflow to tied zero probabilities in the reference
+        ok &= prev_lb - z0 > -80.0f;
+        if (ok) {
+            write_routing_from_row(P, R, row, z0, tok, pe, g.sCnt);
+            return 1;
+        }
+    }
+    // append the candidates as (token, expert) pairs for the exact pair pass
+    int base = 0;
+    if (lane == 0) base = atomicAdd(s_np, n_c);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    int off = 0;
+#pragma unroll
+    for (int jj = 0; jj < J; ++jj) {
+        const bool c = cmask & (1u << jj);
+        const uint32_t m = __ballot_sync(0xffffffffu, c);
+        const int pos = base + off + __popc(m & ((1u << lane) - 1));
+        if (c && pos < kGatePairCap) { g.sPT[pos] = tok; g.sPE[pos] = lane + 32 * jj; }
+        off += __popc(m);
+    }
+    if (base + n_c > kGatePairCap) return 2;
+    if (lane == 0) { g.sTP0[t] = base; g.sTNC[t] = n_c; }
+    return 0;
+}
+
+// Exact reference logits of np (token, expert) pairs: thread p runs pair p's separately-rounded
+// chain over x ascending (gate.hpp:77-81), rows staged through smem in x-chunks (A row and Wg^T row).
+__device__ void gate_pairs_exact(const LaunchParams& P, const RankCtx& R, const float* __restrict__ A,
+                                 const GateSmem& g, int np) {
+    const int H = P.H, tid = threadIdx.x;
+    const int nch = (H + kGatePairX - 1) / kGatePairX;
+    for (int p0 = 0; p0 < np; p0 += kGatePairBatch) {
+        const int nb = min(kGatePairBatch, np - p0);
+        auto load = [&](int st, int ch) {
+            const int x0 = ch * kGatePairX, per_row = min(kGatePairX, H - x0) >> 2;
+            float* b = g.sPair + st * kGatePairBatch * kGatePairPitch;
+            for (int i = tid; i < nb * 2 * per_row; i += kThreads) {
+                const int r = i / per_row, c = i - r * per_row;
+                const int pi = p0 + (r >> 1);
+                const float* src = (r & 1) ? R.wgT + (size_t)g.sPE[pi] * H + x0 + 4 * c
+                                           : A + (size_t)g.sPT[pi] * H + x0 + 4 * c;
+                cp_async16(b + (r >> 1) * kGatePairPitch + (r & 1) * kGatePairX + 4 * c, src, true);
+            }
+            cp_async_commit();
+        };
+        float acc = 0.0f;
+        __syncthreads();
+        load(0, 0);
+        for (int ch = 0; ch < nch; ++ch) {
+            if (ch + 1 < nch) load((ch + 1) & 1, ch + 1); else cp_async_commit();
+            cp_async_wait<1>();
+            __syncthreads();
+            if (tid < nb) {
+                const float* b = g.sPair + (ch & 1) * kGatePairBatch * kGatePairPitch + tid * kGatePairPitch;
+                const int xl = min(kGatePairX, H - ch * kGatePairX);
+                for (int x = 0; x < xl; x += 4) {
+                    const float4 a4 = *reinterpret_cast<const float4*>(b + x);
+                    const float4 w4 = *reinterpret_cast<const float4*>(b + kGatePairX + x);
+                    acc = __fadd_rn(acc, __fmul_rn(a4.x, w4.x));
+                    acc = __fadd_rn(acc, __fmul_rn(a4.y, w4.y));
+                    acc = __fadd_rn(acc, __fmul_rn(a4.z, w4.z));
+                    acc = __fadd_rn(acc, __fmul_rn(a4.w, w4.w));
+                }
+            }
+            __syncthreads();
+        }
+        cp_async_wait<0>();
+        if (tid < nb) g.sPZ[p0 + tid] = acc;
+    }
+    __syncthreads();
+}
+
+// Decide a token from its candidates' exact logits (one warp). false: ties / near-ties -> full exact.
+__device__ bool route_resolve(const LaunchParams& P, const RankCtx& R, float* row, int tok, int t, const GateSmem& g) {
+    const int K = P.k, lane = threadIdx.x & 31;
+    const int n_c = g.sTNC[t], p0 = g.sTP0[t];
+    float zc = -INFINITY;
+    int ec = 0x7fffffff;
+    if (lane < n_c) { zc = g.sPZ[p0 + lane]; ec = g.sPE[p0 + lane]; }
+    if (__any_sync(0xffffffffu, lane < n_c && !(fabsf(zc) < 1e30f))) return false;
+    float m = zc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    int pe[8];
+    bool taken = false, ok = true;
+    float prev = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+        if (j > K || (j == K && n_c == K)) break;
+        float bv = taken ? -INFINITY : zc;
+        int bi = taken ? 0x7fffffff : ec;
+        warp_argmax(bv, bi);
+        if (j > 0) ok &= prev - bv > gate_margin(prev, bv, m);
+        if (j == K) break;
+        if (bi == ec) taken = true;
+        pe[j] = bi;
+        prev = bv;
+    }
+    ok &= prev - m > -80.0f;
+    if (!ok) return false;
+    // exact logits of the candidates replace z~ (G_phi / weights from the row: tolerance)
+    if (lane < n_c) row[ec] = zc;
+    __syncwarp();
+    write_routing_from_row(P, R, row, m, tok, pe, g.sCnt);
+    return true;
+}
+
+__device__ void gate_phase(const LaunchParams& P, const RankCtx& R, const float* __restrict__ A, int cta,
+                           uint8_t* smem, unsigned long long* stat) {
+    const int E = P.E;
+    const int Ep = (E + 7) & ~7;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    constexpr int kWarps = kThreads / 32;
+    GateSmem g;
+    g.sub = gate_sub(Ep);
+    float* region = reinterpret_cast<float*>(smem);
+    g.sL = region;
+    g.sA = g.sL + g.sub * Ep;
+    g.sW = g.sA + kGateStages * g.sub * kGateApitch;
+    g.sPair = g.sL + kGateSubMax * 128 > g.sL + g.sub * Ep ? g.sL + kGateSubMax * 128 : g.sL + g.sub * Ep;
+    uint8_t* tail = smem + ((kGateRegionFloats * 4 + 15) & ~15);
+    g.sNa = reinterpret_cast<double*>(tail);                    tail += kGateSubMax * 8;
+    g.sCnt = reinterpret_cast<int*>(tail);                      tail += kMaxExperts * 4;
+    g.sSab = reinterpret_cast<float*>(tail);                    tail += kGateSubMax * 4;
+    g.sTP0 = reinterpret_cast<int*>(tail);                      tail += kGateSubMax * 4;
+    g.sTNC = reinterpret_cast<int*>(tail);                      tail += kGateSubMax * 4;
+    g.sFull = reinterpret_cast<int*>(tail);                     tail += kGateSubMax * 4;
+    g.sPT = reinterpret_cast<int*>(tail);                       tail += kGatePairCap * 4;
+    g.sPE = reinterpret_cast<int*>(tail);                       tail += kGatePairCap * 4;
+    g.sPZ = reinterpret_cast<float*>(tail);
+    __shared__ int s_np, s_nfull;
+    for (int e = tid; e < Ep; e += kThreads) g.sCnt[e] = 0;
+
+    int tokA, tokB, b0, b1;
+    gate_token_range(P, cta, tokA, tokB, b0, b1);
+    const int ntok = tokB - tokA;
+    const int nsub = (ntok + g.sub - 1) / g.sub;
+    unsigned long long n_full = 0, n_pair_tok = 0;
+
+    for (int si = 0; si < nsub; ++si) {
+        // balanced sub-tiles
+        const int s0 = (int)((long long)ntok * si / nsub);
+        const int s1 = (int)((long long)ntok * (si + 1) / nsub);
+        const int ts = s1 - s0;
+        if (P.exact_gate) {
+            gate_logits<false, kGateTT, kGateTE>(P, R, A, tokA + s0, nullptr, ts, g);
+            for (int t = warp; t < ts; t += kWarps) route_exact(P, R, g.sL + t * Ep, tokA + s0 + t, g.sCnt);
+            n_full += ts;
+            continue;
+        }
+        for (int t = tid; t < ts; t += kThreads) { g.sSab[t] = 0.0f; g.sTNC[t] = 0; }
+        if (tid == 0) { s_np = 0; s_nfull = 0; }
+        __syncthreads();
+        gate_logits<true, kGateTT, kGateTE>(P, R, A, tokA + s0, nullptr, ts, g);
+        for (int t = warp; t < ts; t += kWarps) {
+            const int r = route_certified(P, R, g.sL + t * Ep, tokA + s0 + t, t, g, &s_np);
+            if (r == 2 && (tid & 31) == 0) g.sFull[atomicAdd(&s_nfull, 1)] = tokA + s0 + t;
+        }
+        __syncthreads();
+        const int np = min(s_np, kGatePairCap);
+        if (np > 0 && !(P.debug & kDbgGateNoFlush)) {
+            gate_pairs_exact(P, R, A, g, np);
+            for (int t = warp; t < ts; t += kWarps) {
+                if (g.sTNC[t] == 0) continue;
+                ++n_pair_tok;
+                if (!route_resolve(P, R, g.sL + t * Ep, tokA + s0 + t, t, g) && (tid & 31) == 0)
+                    g.sFull[atomicAdd(&s_nfull, 1)] = tokA + s0 + t;
+            }
+            __syncthreads();
+        }
+        const int nf = s_nfull;
+        if (nf > 0 && !(P.debug & kDbgGateNoFlush)) {   // ties / near-ties / overflow: the reference chain for all E
+            gate_logits<false, 1, 4>(P, R, A, 0, g.sFull, nf, g);
+            for (int t = warp; t < nf; t += kWarps) route_exact(P, R, g.sL + t * Ep, g.sFull[t], g.sCnt);
+            n_full += nf;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) { stat[3] += n_full; }
+    if ((tid & 31) == 0 && n_pair_tok) atomicAdd(&stat[4], n_pair_tok);
+    __syncthreads();
+    for (int e = tid; e < E; e += kThreads) R.cnt_cta[(size_t)cta * E + e] = g.sCnt[e];
 }
 
 // ================================================================ phase 2: slots + dispatch
@@ -833,37 +1234,44 @@ __device__ void gemm_wconvert(const LaunchParams& P, uint8_t* ring, GemmCtrl& G,
 }
 
 // warp 11, one lane: tcgen05.mma issue. One wait (ready) and one commit (done) per stage.
+// kEarlyWait polls stage s+1 before the last MMAs of stage s; with two 64 KB stages the next
+// stage usually lands just in time, so the early poll stalls the tail instead (measured: off).
+constexpr bool kEarlyWait = false;
+constexpr int kTailMmas = 3;
+
 template <int PREC>
-__device__ __forceinline__ void issue_stage(uint32_t d_tmem, uint32_t abase, uint32_t bbase, int kb, int np) {
+struct StageMmas {
+    static constexpr int N = PREC == kFP32 ? 3 * GemmCfg<PREC>::KSTEPS : GemmCfg<PREC>::KSTEPS;
+};
+
+// MMAs [i0, i1) of a stage in issue order (3xTF32: product-major, then k-step).
+template <int PREC>
+__device__ __forceinline__ void issue_stage(uint32_t d_tmem, uint32_t abase, uint32_t bbase, int kb, int np, int i0,
+                                            int i1) {
     using Cfg = GemmCfg<PREC>;
-    if (PREC == kFP32) {
-        // 3xTF32, PRODUCT-major: back-to-back MMAs that read the same TMEM A columns serialize
-        // (measured 61% of peak k-step-major vs 100% product-major)
 #pragma unroll
-        for (int p = 0; p < 3; ++p) {
-            if (p >= np) break;
-#pragma unroll
-            for (int ks = 0; ks < Cfg::KSTEPS; ++ks) {
-                const uint32_t boff = (ks / Cfg::STEPS_PER_ATOM) * Cfg::ATOM_BYTES +
-                                      (ks % Cfg::STEPS_PER_ATOM) * Cfg::KSTEP * Cfg::ESZ;
-                const uint32_t a_hi = abase + ks * Cfg::KSTEP;
-                const uint32_t accum = (kb | ks | p) != 0 ? 1u : 0u;
-                if (np == 1 || p == 2)   // w_hi * x_hi
-                    mma_tf32_ts(d_tmem, a_hi, umma_desc_kmajor(bbase + boff, 128), Cfg::IDESC, accum);
-                else if (p == 0)         // w_lo * x_hi
-                    mma_tf32_ts(d_tmem, a_hi + Cfg::BK, umma_desc_kmajor(bbase + boff, 128), Cfg::IDESC, accum);
-                else                     // w_hi * x_lo
-                    mma_tf32_ts(d_tmem, a_hi, umma_desc_kmajor(bbase + Cfg::PLANE_BYTES + boff, 128), Cfg::IDESC,
-                                accum);
-            }
-        }
-    } else {
-#pragma unroll
-        for (int ks = 0; ks < Cfg::KSTEPS; ++ks) {
-            const uint32_t boff = (ks / Cfg::STEPS_PER_ATOM) * Cfg::ATOM_BYTES +
-                                  (ks % Cfg::STEPS_PER_ATOM) * Cfg::KSTEP * Cfg::ESZ;
+    for (int i = 0; i < StageMmas<PREC>::N; ++i) {
+        if (i < i0 || i >= i1) continue;
+        const int p = PREC == kFP32 ? i / Cfg::KSTEPS : 0;
+        const int ks = PREC == kFP32 ? i % Cfg::KSTEPS : i;
+        if (p >= np) continue;
+        const uint32_t boff = (ks / Cfg::STEPS_PER_ATOM) * Cfg::ATOM_BYTES +
+                              (ks % Cfg::STEPS_PER_ATOM) * Cfg::KSTEP * Cfg::ESZ;
+        const uint32_t accum = (kb | ks | p) != 0 ? 1u : 0u;
+        if (PREC == kFP32) {
+            // product-major: back-to-back MMAs that read the same TMEM A columns serialize
+            // (measured 61% of peak k-step-major vs 100% product-major)
+            const uint32_t a_hi = abase + ks * Cfg::KSTEP;
+            if (np == 1 || p == 2)   // w_hi * x_hi
+                mma_tf32_ts(d_tmem, a_hi, umma_desc_kmajor(bbase + boff, 128), Cfg::IDESC, accum);
+            else if (p == 0)         // w_lo * x_hi
+                mma_tf32_ts(d_tmem, a_hi + Cfg::BK, umma_desc_kmajor(bbase + boff, 128), Cfg::IDESC, accum);
+            else                     // w_hi * x_lo
+                mma_tf32_ts(d_tmem, a_hi, umma_desc_kmajor(bbase + Cfg::PLANE_BYTES + boff, 128), Cfg::IDESC,
+                            accum);
+        } else {
             mma_bf16_ts(d_tmem, abase + ks * (Cfg::KSTEP / 2), umma_desc_kmajor(bbase + boff, 128), Cfg::IDESC,
-                        (kb | ks) != 0 ? 1u : 0u);
+                        accum);
         }
     }
 }
@@ -872,6 +1280,7 @@ template <int PREC>
 __device__ void gemm_mma(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, unsigned long long* trace,
                          unsigned long long* chunklog) {
     using Cfg = GemmCfg<PREC>;
+    constexpr int NM = StageMmas<PREC>::N;
     int nlog = 0;
     long long w_x = 0, w_acc = 0, w_task = 0, ntile = 0;
     int stage = 0;
@@ -895,21 +1304,32 @@ __device__ void gemm_mma(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, unsi
         ++ntile;
         const int nk = ((type == 0 ? P.H : P.D) + Cfg::BK - 1) / Cfg::BK;
         if (!FD_TIMED_WAIT(w_acc, mbar_wait(&G.tempty[acc], accphase ^ 1u, P.abort_flag))) return;
-        tc_fence_after();
         const uint32_t d_tmem = tmem + (uint32_t)(acc * kNT);
+        if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.ready[stage], phase, P.abort_flag))) return;
+        tc_fence_after();
         for (int kb = 0; kb < nk; ++kb) {
-            const long long c0 = clk();
-            if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.ready[stage], phase, P.abort_flag))) return;
-            const long long c1 = clk();
-            tc_fence_after();
-            issue_stage<PREC>(d_tmem, tmem + Cfg::TMEM_A0 + stage * Cfg::A_COLS,
-                              smem_u32(ring + stage * Cfg::STAGE_BYTES), kb, np);
-            mma_commit(&G.done[stage]);   // token + weight stage reusable once these MMAs retire
-            if (chunklog && nlog < kChunkLog) {
-                unsigned long long* e = chunklog + 4 * nlog++;
-                e[0] = c0; e[1] = c1 - c0; e[2] = 0; e[3] = clk() - c1;
+            const uint32_t abase = tmem + Cfg::TMEM_A0 + stage * Cfg::A_COLS;
+            const uint32_t bbase = smem_u32(ring + stage * Cfg::STAGE_BYTES);
+            const int nstage = stage + 1 == Cfg::STAGES ? 0 : stage + 1;
+            const uint32_t nphase = stage + 1 == Cfg::STAGES ? phase ^ 1u : phase;
+            if (kEarlyWait) {
+                issue_stage<PREC>(d_tmem, abase, bbase, kb, np, 0, NM - kTailMmas);
+                if (kb + 1 < nk) {
+                    if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.ready[nstage], nphase, P.abort_flag))) return;
+                    tc_fence_after();
+                }
+                issue_stage<PREC>(d_tmem, abase, bbase, kb, np, NM - kTailMmas, NM);
+            } else {
+                issue_stage<PREC>(d_tmem, abase, bbase, kb, np, 0, NM);
             }
-            if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
+            mma_commit(&G.done[stage]);   // token + weight stage reusable once these MMAs retire
+            if (chunklog && nlog < kChunkLog) chunklog[4 * nlog++] = clk();
+            stage = nstage;
+            phase = nphase;
+            if (!kEarlyWait && kb + 1 < nk) {
+                if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.ready[stage], phase, P.abort_flag))) return;
+                tc_fence_after();
+            }
         }
         mma_commit(&G.tfull[acc]);         // accumulator ready for the epilogue
         if (++acc == kAccStages) { acc = 0; accphase ^= 1u; }
@@ -1137,9 +1557,9 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
     const float* A = P.in[rl];
     float* O = P.out[rl];
     const int tid = threadIdx.x, warp = tid >> 5;
-    __shared__ unsigned long long s_stat[4];
+    __shared__ unsigned long long s_stat[5];   // gemm0/gemm1 tiles, combine tasks, full-exact / pair-resolved gate tokens
     __shared__ int s_n_expert[kMaxExperts];   // kept rows per expert of this rank (dispatch -> combine)
-    if (tid < 4) s_stat[tid] = 0;
+    if (tid < 5) s_stat[tid] = 0;
     unsigned long long* trace = R.trace + (size_t)cta * kTracePts;
     if (tid == 0) trace[0] = globaltimer();
 
@@ -1163,7 +1583,7 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
     const uint32_t tmem_base = G.tmem_base;
 
     // phase 1: exact gate (uses the smem region as scratch)
-    gate_phase(P, R, A, cta, smem);
+    gate_phase(P, R, A, cta, smem, s_stat);
     if (tid == 0) trace[1] = globaltimer();
     if (!rank_barrier(P, R, P.launch_seq)) goto done;
     if (tid == 0) trace[2] = globaltimer();
@@ -1217,6 +1637,8 @@ done:
         atomicAdd(R.stats + 0, s_stat[0]);
         atomicAdd(R.stats + 1, s_stat[1]);
         atomicAdd(R.stats + 2, s_stat[2]);
+        atomicAdd(R.stats + 3, s_stat[3]);
+        atomicAdd(R.stats + 4, s_stat[4]);
     }
 }
 
@@ -1304,7 +1726,7 @@ __global__ void __launch_bounds__(kThreads, 1) debug_gemm_kernel(const __grid_co
             mbar_wait(&G.ready[stage], phase, abort_flag);
             tc_fence_after();
             issue_stage<PREC>(tmem, tmem + Cfg::TMEM_A0 + stage * Cfg::A_COLS, smem_u32(smem + stage * Cfg::STAGE_BYTES),
-                              kb, 3);
+                              kb, 3, 0, StageMmas<PREC>::N);
             mma_commit(&G.done[stage]);
             if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
         }

@@ -103,7 +103,7 @@ struct RankRes {
     void* c1[2] = {nullptr, nullptr};
     void* w1[2] = {nullptr, nullptr};
     void* w2[2] = {nullptr, nullptr};
-    float *b1 = nullptr, *b2 = nullptr, *wg = nullptr;
+    float *b1 = nullptr, *b2 = nullptr, *wg = nullptr, *wg_norm = nullptr, *wgT = nullptr;
     float* g_phi = nullptr;
     int32_t *pick_e = nullptr, *pick_slot = nullptr;
     float* pick_w = nullptr;
@@ -190,6 +190,8 @@ fdmoe_status alloc_rank(fdmoe_handle* h, RankRes& r, int ctas_per_rank) {
     parts.push_back({(void**)&r.b1, (size_t)d.El * d.D * 4});
     parts.push_back({(void**)&r.b2, (size_t)d.El * d.H * 4});
     parts.push_back({(void**)&r.wg, (size_t)d.H * d.E * 4});
+    parts.push_back({(void**)&r.wg_norm, (size_t)d.E * 4});
+    parts.push_back({(void**)&r.wgT, (size_t)d.E * d.H * 4});
     parts.push_back({(void**)&r.g_phi, (size_t)d.S * d.E * 4});
     parts.push_back({(void**)&r.pick_e, (size_t)d.S * d.k * 4});
     parts.push_back({(void**)&r.pick_slot, (size_t)d.S * d.k * 4});
@@ -243,7 +245,7 @@ fdmoe_status build_ctx(fdmoe_handle* h) {
             c.hl = r.hl;
             c.c1[0] = r.c1[0];
             c.c1[1] = r.c1[d.planes - 1];
-            c.b1 = r.b1; c.b2 = r.b2; c.wg = r.wg;
+            c.b1 = r.b1; c.b2 = r.b2; c.wg = r.wg; c.wg_norm = r.wg_norm; c.wgT = r.wgT;
             c.g_phi = r.g_phi; c.pick_e = r.pick_e; c.pick_slot = r.pick_slot; c.pick_w = r.pick_w;
             c.cnt_cta = r.cnt_cta; c.tbl_tok = r.tbl_tok; c.tbl_w = r.tbl_w; c.slot_counts = r.slot_counts;
             c.blk_ready = r.blk_ready;
@@ -443,6 +445,29 @@ fdmoe_status fdmoe_set_weights(fdmoe_handle* h, const float* wg, const float* w1
     if (!wg || !w1 || !b1 || !w2 || !b2) return fail(FDMOE_ERR_CONFIG, "null weight pointer");
     const Dims& d = h->dm;
     const cudaMemcpyKind kind = where == FDMOE_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    // |Wg[:, e]|_2 for the certified gate, computed in double and rounded up to float
+    std::vector<float> wn(d.E), wt((size_t)d.E * d.H);
+    {
+        std::vector<float> hw;
+        const float* src = wg;
+        if (where != FDMOE_HOST) {
+            hw.resize((size_t)d.H * d.E);
+            CK(cudaMemcpy(hw.data(), wg, hw.size() * 4, cudaMemcpyDeviceToHost));
+            src = hw.data();
+        }
+        std::vector<double> ss(d.E, 0.0);
+        for (int64_t x = 0; x < d.H; ++x)
+            for (int64_t e = 0; e < d.E; ++e) {
+                ss[e] += (double)src[x * d.E + e] * src[x * d.E + e];
+                wt[e * d.H + x] = src[x * d.E + e];
+            }
+        for (int64_t e = 0; e < d.E; ++e) {
+            const double n = std::sqrt(ss[e]) * (1.0 + 1e-12);
+            float f = (float)n;
+            if ((double)f < n) f = std::nextafter(f, INFINITY);
+            wn[e] = f;
+        }
+    }
     for (auto& r : h->ranks) {
         CK(cudaSetDevice(r.dev));
         const int64_t e0 = (int64_t)r.rank * d.El;   // config.hpp:66 uniform placement
@@ -459,6 +484,8 @@ fdmoe_status fdmoe_set_weights(fdmoe_handle* h, const float* wg, const float* w1
         CK(cudaMemcpy(r.b1, b1 + e0 * d.D, (size_t)d.El * d.D * 4, kind));
         CK(cudaMemcpy(r.b2, b2 + e0 * d.H, (size_t)d.El * d.H * 4, kind));
         CK(cudaMemcpy(r.wg, wg, (size_t)d.H * d.E * 4, kind));
+        CK(cudaMemcpy(r.wg_norm, wn.data(), (size_t)d.E * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(r.wgT, wt.data(), wt.size() * 4, cudaMemcpyHostToDevice));
     }
     h->weights_set = true;
     return FDMOE_OK;
@@ -492,6 +519,12 @@ static fdmoe_status launch_all(fdmoe_handle* h, const float* const* in_dev, floa
         p.budget_ns = (unsigned long long)budget_ms * 1000000ull;
         p.abort_flag = g.d_abort;
         p.sequential = 0;
+        p.exact_gate = (opts && opts->exact_gate) ? 1 : 0;
+        {   // certified-gate bound coefficients (fdmoe_kernel.cu, phase 1)
+            const double u = std::ldexp(1.0, -24), n1 = (double)d.H + 1.0;
+            p.gate_u = (float)(u * 1.001);
+            p.gate_k1 = (float)((66.0 + 2.0 * (double)d.H * (n1 * u / (1.0 - n1 * u))) * 1.001);
+        }
         const char* dbg = getenv("FDMOE_DEBUG");   // ablation switches (tools/ablate.py); unset in production
         p.debug = dbg ? atoi(dbg) : 0;
         CK(cudaSetDevice(g.dev));
@@ -507,9 +540,9 @@ static fdmoe_status launch_all(fdmoe_handle* h, const float* const* in_dev, floa
 }
 
 fdmoe_status fdmoe_forward_async(fdmoe_handle* h, const float* const* in_dev, float* const* out_dev,
-                                 void* const* streams) {
+                                 void* const* streams, const fdmoe_options* opts) {
     if (!h || !in_dev || !out_dev) return fail(FDMOE_ERR_CONFIG, "null argument");
-    return launch_all(h, in_dev, out_dev, streams, nullptr);
+    return launch_all(h, in_dev, out_dev, streams, opts);
 }
 
 fdmoe_status fdmoe_sync(fdmoe_handle* h) {
@@ -605,6 +638,8 @@ fdmoe_status fdmoe_forward(fdmoe_handle* h, const float* const* in_shards, float
             so.bound_final = so.executed;
             so.bound_initial = d.El * d.MT * (d.NB0 + d.NB1) + (d.S + kCombineTok - 1) / kCombineTok;
             so.launches = 1;
+            so.gate_exact_tokens = (int64_t)(s1[3] - stat0[i * 8 + 3]);
+            so.gate_pair_tokens = (int64_t)(s1[4] - stat0[i * 8 + 4]);
             for (auto& g : h->groups)
                 if (g.dev == r.dev) {
                     float ms = 0.0f;

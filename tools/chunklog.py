@@ -16,7 +16,4 @@ fd._check(fd.lib().fdmoe_read_chunklog(op._h, fd._ptr(lg)))
 lg = lg.astype(np.int64)
 d = np.diff(lg[:, 0])
 print("chunk period (cycles): median", np.median(d[:200]), "mean", d[:200].mean())
-print("wait ready median", np.median(lg[:200, 1]), " issue median", np.median(lg[:200, 3]))
-print("first 70 chunks: period / wX / wA / issue")
-for i in range(60, 130):
-    print(i, d[i], lg[i, 1], lg[i, 2], lg[i, 3])
+print("periods 60..130:", list(d[60:130]))
