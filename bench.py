@@ -226,10 +226,9 @@ def main():
     model = fd.make_model(cfg)
     shards_all = fd.make_shards(cfg)
     if world > 1:
+        from paper_2506_04667_b200 import dist as fdist
         op = fd.Operator(cfg, device_ids=[local], first_rank=rank, n_local=1)
-        blobs = [None] * world
-        dist.all_gather_object(blobs, op.export_heap())
-        op.import_peers(blobs)
+        fdist.attach_peers(op)   # bootstrap only: CUDA-IPC heap handles, rank-major
         my = [shards_all[rank]]
     else:
         op = fd.Operator(cfg, device_ids=[0] * n)   # n == 1 here (or virtual ranks if --gpus > 1 w/o torchrun)
@@ -269,9 +268,7 @@ def main():
     op.sync()
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = fdist.max_over_ranks(ms, device="cuda")
     tokens_per_step = cfg.tokens_per_device * n
     value = tokens_per_step / (ms * 1e-3)
     # cross-check: the operator's own events around its launches (same stream)
@@ -288,9 +285,7 @@ def main():
         _forward_host(fd, op, host_in, outs_h)
     e2e_s = (time.perf_counter() - t0) / args.e2e_steps
     if world > 1:
-        t = torch.tensor([e2e_s], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+        e2e_s = fdist.max_over_ranks(e2e_s, device="cuda")
     e2e = {"value": tokens_per_step / e2e_s, "unit": "tokens/s",
            "h2d_bytes_per_step": int(sum(x.nbytes for x in host_in)),
            "d2h_bytes_per_step": int(sum(x.nbytes for x in outs_h)), "ms_per_step": e2e_s * 1e3}

@@ -162,7 +162,8 @@ fdmoe_status fdmoe_import_peers(fdmoe_handle* h, const void* blobs, int32_t worl
 
 /* ModelWeights (config.hpp:130-147) for all E_total experts; each local rank uploads
  * its own E_local experts (device p owns [p*E_local, (p+1)*E_local), config.hpp:66) and
- * repacks them K-major (and tf32 hi/lo or bf16) once. Layouts as fdmoe_synth_model. */
+ * repacks them K-major once (FP32, split into tf32 hi/lo on chip per tile; or bf16).
+ * Also precomputes |Wg[:, e]| and Wg^T for the certified gate. Layouts as fdmoe_synth_model. */
 fdmoe_status fdmoe_set_weights(fdmoe_handle* h, const float* wg, const float* w1, const float* b1,
                                const float* w2, const float* b2, int32_t where);
 

@@ -10,9 +10,10 @@
 //     moefabric::ForwardResult r = moefabric::forward(cfg, shards, model, opts);
 //
 // Differences, all documented in INTEGRATION.md: ForwardResult::trace is empty (device
-// evidence comes from ncu), TaskStats count 128x256 GPU tiles instead of bM x bN CPU
-// tasks, MoeConfig gains `precision` (FP32-accurate 3xTF32 by default), and
-// ForwardOptions gains `device_ids` (default: every rank on GPU 0 = virtual ranks).
+// evidence comes from ncu and fdmoe_read_trace), TaskStats count 128x128 GPU tiles instead of
+// bM x bN CPU tasks, MoeConfig gains `precision` (FP32-accurate 3xTF32 by default), and
+// ForwardOptions gains `device_ids` (default: every rank on GPU 0 = virtual ranks) and
+// `exact_gate` (default false: certified gate — routing bit-exact, G_phi within ~1e-6).
 #pragma once
 
 #include <cmath>

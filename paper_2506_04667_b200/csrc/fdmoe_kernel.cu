@@ -939,10 +939,11 @@ __device__ void dispatch_phase(const LaunchParams& P, const RankCtx& R, const fl
 // ================================================================ phase 3: expert FFN
 // Tile = (local expert le, feature block nb of 128 outputs, row tile m of 128 received tokens):
 //   D[f][t] = sum_k W^T[f][k] * X[t][k]     (GEMM0: K = H, W = W1;  GEMM1: K = D, W = W2, X = C1)
-// A operand (weights) lives in TMEM: loader warps read FP32 rows with coalesced 16-byte loads,
-// split them into tf32 hi/lo in registers and tcgen05.st both parts into a 4-stage TMEM ring —
-// weights cross HBM once at 4 bytes/element. B operand (tokens, already hi/lo-split at dispatch)
-// is TMA-staged in a SWIZZLE_128B smem ring. 3xTF32: lo*hi + hi*lo + hi*hi per k-step, FP32
+// A operand (weights) lives in TMEM: the producer TMA-loads raw FP32 (or bf16) weight rows into a
+// SWIZZLE_128B smem ring; 4 converter warps read them (LDS), split FP32 into tf32 hi/lo in
+// registers and tcgen05.st both parts into the TMEM stage — weights cross HBM once at 4 bytes per
+// element. B operand (tokens, already hi/lo-split by the sender at dispatch) is TMA-staged in a
+// SWIZZLE_128B smem ring. 3xTF32: lo*hi + hi*lo + hi*hi per k-step (product-major), FP32
 // accumulation in double-buffered TMEM accumulators. (runtime.hpp:652-699, tiled_blas.hpp:80-96)
 struct Task {
     int type;   // 0 = GEMM0, 1 = GEMM1, -1 = end
