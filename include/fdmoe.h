@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define FDMOE_ABI_VERSION 1
+#define FDMOE_ABI_VERSION 2
 
 typedef enum fdmoe_status {
     FDMOE_OK = 0,
@@ -73,17 +73,35 @@ typedef struct fdmoe_config {
     uint64_t seed;
 } fdmoe_config;
 
-/* ForwardOptions (runtime.hpp:86-92). processors/mode/straggler are accepted for source
- * compatibility; on the GPU the persistent launch uses every co-resident CTA. */
+/* StragglerSpec::Kind (runtime.hpp:78-84) */
+typedef enum fdmoe_straggler_kind {
+    FDMOE_STRAGGLER_NONE = 0,
+    FDMOE_STRAGGLER_CONSTANT = 1,  /* a = delay ms per packet */
+    FDMOE_STRAGGLER_UNIFORM = 2,   /* U(a, b) ms per packet */
+    FDMOE_STRAGGLER_LOGNORMAL = 3  /* lognormal(log a, b) ms per packet */
+} fdmoe_straggler_kind;
+
+/* ForwardOptions (runtime.hpp:86-92). `processors` is accepted for source compatibility; on the
+ * GPU the persistent launch uses every co-resident CTA. */
 typedef struct fdmoe_options {
     int32_t processors;         /* reference processor threads per device (ignored) */
-    int32_t sequential;         /* ScheduleMode::sequential (bulk-synchronous baseline) */
+    int32_t sequential;         /* ScheduleMode::sequential: bulk-synchronous baseline inside the
+                                 * same launch — gate+dispatch | group barrier | expert FFN |
+                                 * group barrier | combine (runtime.hpp:885-908) */
     int64_t deadlock_budget_ms; /* in-kernel watchdog budget (runtime.hpp:90, default 5000) */
     int32_t exact_gate;         /* 1: reference-exact gate logits for every token (G_phi and
                                  * combine weights bit-identical to the reference); 0 (default):
                                  * certified gate — FFMA logits, routing (assignment, slots, drops)
                                  * proven identical per token, exact recompute where unproven */
-    int32_t reserved;
+    int32_t trace_events;       /* 1: record the device event log (fdmoe_read_events) */
+    /* StragglerSpec (runtime.hpp:78-84): rank `straggler_device` holds back each of its dispatch
+     * packet signals by a delay sampled per packet, in the reference's order and RNG stream
+     * (runtime.hpp:312-326, 341-362); delays accumulate as the reference's sleeps do. */
+    int32_t straggler_kind;     /* fdmoe_straggler_kind */
+    int32_t straggler_device;
+    double straggler_a;
+    double straggler_b;
+    uint64_t seed;              /* ForwardOptions::seed (straggler sampling) */
 } fdmoe_options;
 
 /* Per-rank routing surface (GateOutput, gate.hpp:24-37). All host pointers, nullable.
@@ -138,6 +156,12 @@ int32_t fdmoe_validate_write(int64_t src, int64_t dst, int64_t p_star, int64_t b
 int64_t fdmoe_gemm_tasks_for_rows(const fdmoe_config* cfg, int64_t rows);
 int64_t fdmoe_combine_tiles_for_rows(const fdmoe_config* cfg, int64_t rows);
 int64_t fdmoe_initial_task_bound(const fdmoe_config* cfg);
+
+/* StragglerSpec sampling (runtime.hpp:312-326, 341-362): cum_ns[devices * local_experts] = running
+ * sum of the per-packet delays the straggler device would sleep, in the reference's packet order and
+ * RNG stream; packet e's dispatch signal is held back by cum_ns[e] after dispatch starts. */
+fdmoe_status fdmoe_straggler_delays(const fdmoe_options* opts, int64_t devices, int64_t local_experts,
+                                    uint64_t* cum_ns);
 
 /* Seeded synthetic model / shards, restating harness.hpp:76-109 bit for bit
  * (std::mt19937_64 + std::normal_distribution<float>). Layouts: wg H x E; w1 E x H x D;
@@ -205,6 +229,30 @@ fdmoe_status fdmoe_last_kernel_ms(fdmoe_handle* h, double* ms);
  * resolving tiles; epilogue busy cycles; FFN tiles issued by the MMA warp.
  * Writes min(cap/20, ctas) rows, then clears. */
 fdmoe_status fdmoe_read_trace(fdmoe_handle* h, int32_t local_rank, uint64_t* out, int32_t cap, int32_t* n_ctas);
+/* Device event log of the most recent launch with opts->trace_events (the reference's TraceEvent
+ * stream, trace.hpp:17-60, recorded by the kernel with %globaltimer ns). One record per event: */
+typedef enum fdmoe_event_kind {
+    FDMOE_EV_SPAWN = 0,          /* per CTA: t0 = kernel start, t1 = exit */
+    FDMOE_EV_GATE_DONE = 1,      /* per CTA: t0 = start, t1 = its gate tokens routed */
+    FDMOE_EV_DISPATCH_PUT = 2,   /* packet signal published: src = this rank, peer = owner,
+                                  * expert = owner-local expert, value = rows (pgas put) */
+    FDMOE_EV_EXEC = 3,           /* task executed [t0, t1]: type 1 gemm0 / 2 gemm1 (expert, rb = row
+                                  * tile, cb = feature block, src = first source packet, peer =
+                                  * packets in the tile, value = rows) or 3 combine (rb = token block) */
+    FDMOE_EV_TILE_PUT = 4,       /* GEMM1 tile stored into origin `peer`'s combine buffer and
+                                  * signalled: expert, rb = row tile, cb, value = rows */
+    FDMOE_EV_BARRIER_ENTER = 5,  /* sequential mode group barrier (value = barrier id) */
+    FDMOE_EV_BARRIER_EXIT = 6
+} fdmoe_event_kind;
+typedef struct fdmoe_event {
+    uint64_t t0, t1;
+    int32_t kind, cta, type, src, expert, rb, cb, peer;
+    int64_t value;
+} fdmoe_event;
+/* Copies up to `cap` records of local rank `local_rank`; *n = events recorded (may exceed cap or
+ * the device buffer; *dropped = records lost to the device buffer's capacity). */
+fdmoe_status fdmoe_read_events(fdmoe_handle* h, int32_t local_rank, fdmoe_event* out, int64_t cap, int64_t* n,
+                               int64_t* dropped);
 
 /* ---- diagnostics (tests only; not part of the reference surface) -------------------- */
 /* The kernel's glibc-expf restatement on n host floats (runs on device 0). */

@@ -16,7 +16,9 @@
 // `exact_gate` (default false: certified gate — routing bit-exact, G_phi within ~1e-6).
 #pragma once
 
+#include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -209,13 +211,36 @@ struct ForwardOptions {
     std::uint64_t seed = 0;
     std::vector<std::int32_t> device_ids;   // B200 addition: CUDA device per rank (default all 0)
     bool exact_gate = false;                // B200 addition: reference-exact gate logits (fdmoe.h)
+    bool trace = true;                      // B200 addition: record the device event log into ForwardResult::trace
 };
 struct TaskStats {
     std::int64_t gemm0 = 0, gemm1 = 0, combine = 0, enqueued = 0, executed = 0;
     std::int64_t bound_initial = 0, bound_final = 0, scheduled_final = 0, launches = 0;
     std::int64_t total() const { return gemm0 + gemm1 + combine; }
 };
-struct TraceEvent {};
+// trace.hpp:38-60, recorded on the device (fdmoe_read_events); t0/t1 are ns since the earliest
+// event of the launch (%globaltimer), `worker` is the CTA ("cta<N>").
+struct TraceEvent {
+    std::uint64_t t0 = 0, t1 = 0;
+    std::int32_t device = -1;
+    char worker[12] = {0};
+    const char* event = "";
+    const char* task_type = nullptr;  // "gemm0" | "gemm1" | "combine"
+    std::int32_t src = -1, expert = -1, rb = -1, cb = -1;
+    std::int64_t value = -1;
+    std::int32_t peer = -1;
+    bool has_task() const { return task_type != nullptr; }
+};
+namespace detail {
+inline const char* event_name(std::int32_t k) {
+    static const char* names[] = {"spawn", "gate_done", "dispatch_put", "exec", "tile_put", "barrier_enter",
+                                  "barrier_exit"};
+    return (k >= 0 && k < 7) ? names[k] : "unknown";
+}
+inline const char* task_name(std::int32_t t) {
+    return t == 1 ? "gemm0" : t == 2 ? "gemm1" : t == 3 ? "combine" : nullptr;
+}
+}  // namespace detail
 struct ForwardResult {
     std::vector<TokenMatrix> outputs;
     std::vector<GateOutput> gates;
@@ -294,7 +319,41 @@ inline ForwardResult forward(const MoeConfig& cfg, const std::vector<TokenMatrix
     o.sequential = opts.mode == ScheduleMode::sequential ? 1 : 0;
     o.deadlock_budget_ms = opts.deadlock_budget_ms;
     o.exact_gate = opts.exact_gate ? 1 : 0;
+    o.trace_events = opts.trace ? 1 : 0;
+    o.straggler_kind = static_cast<std::int32_t>(opts.straggler.kind);
+    o.straggler_device = opts.straggler.device;
+    o.straggler_a = opts.straggler.a;
+    o.straggler_b = opts.straggler.b;
+    o.seed = opts.seed;
     detail::check(fdmoe_forward(h, in.data(), out.data(), FDMOE_HOST, &o, ro.data(), st.data()));
+    if (opts.trace) {
+        std::vector<fdmoe_event> evs;
+        std::uint64_t base = ~0ull;
+        for (std::int64_t d = 0; d < P; ++d) {
+            std::int64_t n = 0, dropped = 0;
+            detail::check(fdmoe_read_events(h, static_cast<std::int32_t>(d), nullptr, 0, &n, &dropped));
+            std::vector<fdmoe_event> buf(static_cast<std::size_t>(n));
+            detail::check(fdmoe_read_events(h, static_cast<std::int32_t>(d), buf.data(), n, &n, &dropped));
+            for (auto& e : buf) {
+                base = std::min<std::uint64_t>(base, e.t0);
+                res.trace.emplace_back();
+                TraceEvent& t = res.trace.back();
+                t.t0 = e.t0;
+                t.t1 = e.t1;
+                t.device = static_cast<std::int32_t>(d);
+                std::snprintf(t.worker, sizeof(t.worker), "cta%d", e.cta);
+                t.event = detail::event_name(e.kind);
+                t.task_type = e.kind == FDMOE_EV_EXEC ? detail::task_name(e.type) : nullptr;
+                t.src = e.src; t.expert = e.expert; t.rb = e.rb; t.cb = e.cb; t.value = e.value; t.peer = e.peer;
+            }
+        }
+        for (auto& t : res.trace) {
+            t.t0 -= base;
+            if (t.t1) t.t1 -= base;
+        }
+        std::stable_sort(res.trace.begin(), res.trace.end(),
+                         [](const TraceEvent& a, const TraceEvent& b) { return a.t0 < b.t0; });
+    }
 
     double kernel_ms = 0.0;
     for (std::int64_t d = 0; d < P; ++d) {

@@ -87,6 +87,8 @@ def ref():
         L.ref_gate.argtypes = [vp, C.c_double, i64, vp, vp, vp, vp, vp, vp, vp, vp]
         L.ref_expert_capacity.restype = i64
         L.ref_expert_capacity.argtypes = [vp, C.c_double]
+        L.ref_straggler_delays.restype = i32
+        L.ref_straggler_delays.argtypes = [i32, C.c_double, C.c_double, i32, C.c_uint64, i64, i64, vp]
         _ref = L
     return _ref
 
@@ -201,3 +203,11 @@ def ref_gate(cfg, a, wg, cap: int = -1):
         raise RuntimeError(ref().ref_last_error().decode())
     return dict(g_phi=g, table_token=tt, table_weight=tw, slot_counts=sc,
                 dropped=[(int(dr[2 * i]), int(dr[2 * i + 1])) for i in range(int(nd[0]))])
+
+
+def ref_straggler_delays(kind: int, a: float, b: float, device: int, seed: int, devices: int,
+                         local_experts: int) -> np.ndarray:
+    """The reference's own sample_delay_ms draws (runtime.hpp:312-362), cumulative ms per packet."""
+    out = np.zeros(devices * local_experts, np.float64)
+    ref().ref_straggler_delays(kind, a, b, device, seed, devices, local_experts, _p(out))
+    return out

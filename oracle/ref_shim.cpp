@@ -170,4 +170,24 @@ int ref_gate(const int64_t* cfgv, double cf, int64_t cap, const float* a, const 
 
 int64_t ref_expert_capacity(const int64_t* cfgv, double cf) { return expert_capacity(make_cfg(cfgv, cf)); }
 
+// The reference's own per-packet straggler draws (runtime.hpp:312-326) in dispatch_tokens' order
+// and RNG seeding (runtime.hpp:341-362), accumulated in ms: cum_ms[t * E_local + le].
+int ref_straggler_delays(int kind, double a, double b, int device, uint64_t seed, int64_t devices,
+                         int64_t local_experts, double* cum_ms) {
+    StragglerSpec sp;
+    sp.kind = static_cast<StragglerSpec::Kind>(kind);
+    sp.a = a;
+    sp.b = b;
+    sp.device = device;
+    std::mt19937_64 rng(seed ^ (0x9E3779B97F4A7C15ull * (static_cast<std::uint64_t>(device) + 1)));
+    double cum = 0.0;
+    for (int64_t t = 0; t < devices; ++t)
+        for (int64_t le = 0; le < local_experts; ++le) {
+            const double ms = moefabric::detail::sample_delay_ms(sp, rng);
+            if (ms > 0.0) cum += ms;
+            cum_ms[t * local_experts + le] = cum;
+        }
+    return 0;
+}
+
 }  // extern "C"

@@ -91,7 +91,9 @@ class _Cfg(C.Structure):
 
 class _Opts(C.Structure):
     _fields_ = [("processors", C.c_int32), ("sequential", C.c_int32), ("deadlock_budget_ms", C.c_int64),
-                ("exact_gate", C.c_int32), ("reserved", C.c_int32)]
+                ("exact_gate", C.c_int32), ("trace_events", C.c_int32), ("straggler_kind", C.c_int32),
+                ("straggler_device", C.c_int32), ("straggler_a", C.c_double), ("straggler_b", C.c_double),
+                ("seed", C.c_uint64)]
 
 
 class _Routing(C.Structure):
@@ -120,6 +122,7 @@ EXPORTED_SYMBOLS = [
     "fdmoe_synth_model", "fdmoe_synth_shards", "fdmoe_create", "fdmoe_destroy", "fdmoe_ipc_size",
     "fdmoe_export_heap", "fdmoe_import_peers", "fdmoe_set_weights", "fdmoe_forward", "fdmoe_forward_async",
     "fdmoe_sync", "fdmoe_get_info", "fdmoe_last_kernel_ms", "fdmoe_read_trace", "fdmoe_debug_expf", "fdmoe_debug_gemm", "fdmoe_debug_mma_rate", "fdmoe_debug_latency", "fdmoe_read_chunklog",
+    "fdmoe_read_events", "fdmoe_straggler_delays",
 ]
 
 _LIB = None
@@ -170,6 +173,8 @@ def lib():
         "fdmoe_debug_mma_rate": (i32, [i32, i32, i32, i32, vp]),
         "fdmoe_debug_latency": (i32, [i32, vp]),
         "fdmoe_read_chunklog": (i32, [vp, vp]),
+        "fdmoe_read_events": (i32, [vp, i32, vp, i64, vp, vp]),
+        "fdmoe_straggler_delays": (i32, [C.POINTER(_Opts), i64, i64, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -219,6 +224,29 @@ class MoeConfig:
         _check(lib().fdmoe_config_validate(C.byref(c), 1 if gpu_envelope else 0))
 
 
+class ScheduleMode:
+    """runtime.hpp:76."""
+    overlapped = "overlapped"
+    sequential = "sequential"
+
+
+@dataclasses.dataclass
+class StragglerSpec:
+    """runtime.hpp:78-84: kind none | constant (a ms) | uniform (U(a, b) ms) | lognormal (median a ms,
+    sigma b), applied per dispatch packet of rank `device`."""
+    kind: str = "none"
+    a: float = 0.0
+    b: float = 0.0
+    device: int = 0
+
+    _KINDS = {"none": 0, "constant": 1, "uniform": 2, "lognormal": 3}
+
+    def kind_code(self) -> int:
+        if self.kind not in self._KINDS:
+            raise ConfigError(f"unknown straggler kind {self.kind!r}")
+        return self._KINDS[self.kind]
+
+
 @dataclasses.dataclass
 class ForwardOptions:
     """runtime.hpp:86-92."""
@@ -229,10 +257,21 @@ class ForwardOptions:
     # B200 addition: True = reference-exact gate logits for every token (G_phi and combine weights
     # bit-identical); False = certified gate (routing proven identical per token)
     exact_gate: bool = False
+    mode: str = ScheduleMode.overlapped
+    straggler: StragglerSpec = dataclasses.field(default_factory=StragglerSpec)
+    # B200 addition: record the device event log into ForwardResult.trace (trace.py / audit.py)
+    trace: bool = False
+
+    def is_sequential(self) -> bool:
+        if self.mode not in (ScheduleMode.overlapped, ScheduleMode.sequential):
+            raise ConfigError(f"unknown schedule mode {self.mode!r}")
+        return bool(self.sequential) or self.mode == ScheduleMode.sequential
 
     def to_c(self):
-        return _Opts(self.processors, 1 if self.sequential else 0, self.deadlock_budget_ms,
-                     1 if self.exact_gate else 0, 0)
+        sp = self.straggler
+        return _Opts(self.processors, 1 if self.is_sequential() else 0, self.deadlock_budget_ms,
+                     1 if self.exact_gate else 0, 1 if self.trace else 0, sp.kind_code(), sp.device,
+                     float(sp.a), float(sp.b), self.seed)
 
 
 @dataclasses.dataclass
@@ -289,7 +328,8 @@ class TaskStats:
 
 @dataclasses.dataclass
 class ForwardResult:
-    """runtime.hpp:108-117. `trace` is empty on the GPU path (evidence comes from ncu)."""
+    """runtime.hpp:108-117. `trace` holds the device event log (trace.TraceEvent list, trace.hpp:38-60)
+    when ForwardOptions.trace is set, else []."""
     outputs: List[np.ndarray]
     gates: List[GateOutput]
     manifests: List[DispatchManifest]
@@ -340,6 +380,15 @@ def combine_tiles_for_rows(cfg: MoeConfig, n: int) -> int:
 def initial_task_bound(cfg: MoeConfig) -> int:
     c = cfg.to_c()
     return int(lib().fdmoe_initial_task_bound(C.byref(c)))
+
+
+def straggler_delays(cfg: MoeConfig, opts: ForwardOptions) -> np.ndarray:
+    """Cumulative per-packet hold-back (ns) of the straggler's dispatch signals (runtime.hpp:312-362):
+    entry e = destination * E_local + local expert."""
+    out = np.zeros(cfg.experts_total, np.uint64)
+    o = opts.to_c()
+    _check(lib().fdmoe_straggler_delays(C.byref(o), cfg.devices, cfg.local_experts(), _ptr(out)))
+    return out
 
 
 def make_model(cfg: MoeConfig, seed: Optional[int] = None) -> ModelWeights:
@@ -505,7 +554,11 @@ class Operator:
             b = payload_bytes(cfg, [g.slot_counts for g in gates])
         else:
             b = np.zeros(cfg.devices * cfg.devices, np.uint64)
-        return ForwardResult(outs, gates, manifests, [], b, padded_baseline_bytes(cfg), stats_l, t1 - t0)
+        tr = []
+        if o.trace:
+            from . import trace as _trace
+            tr = _trace.to_trace_events([self.events(i) for i in range(n)], first_rank=self.first_rank)
+        return ForwardResult(outs, gates, manifests, tr, b, padded_baseline_bytes(cfg), stats_l, t1 - t0)
 
     def forward_device(self, in_ptrs: Sequence[int], out_ptrs: Sequence[int], streams: Optional[Sequence[int]] = None,
                        opts: Optional[ForwardOptions] = None):
@@ -531,6 +584,18 @@ class Operator:
         t0 = t[:, 0].min()
         t[:, :7] -= t0
         return t
+
+    def events(self, local_rank: int = 0) -> np.ndarray:
+        """Device event log of the most recent launch run with ForwardOptions(trace=True), as a
+        structured array (trace.EVENT_DTYPE, raw %globaltimer ns). Raises if records were lost."""
+        from .trace import EVENT_DTYPE
+        n, dropped = C.c_int64(), C.c_int64()
+        _check(lib().fdmoe_read_events(self._h, local_rank, None, 0, C.byref(n), C.byref(dropped)))
+        buf = np.zeros(n.value, EVENT_DTYPE)
+        _check(lib().fdmoe_read_events(self._h, local_rank, _ptr(buf), n.value, C.byref(n), C.byref(dropped)))
+        if dropped.value:
+            raise RuntimeFault(f"event log overflow: {dropped.value} records lost")
+        return buf
 
     def last_kernel_ms(self) -> float:
         """Device time of the most recent layer launch (CUDA events around it, max over devices)."""

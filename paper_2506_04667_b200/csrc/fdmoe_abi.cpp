@@ -1,6 +1,7 @@
 // fdmoe_abi.cpp — the GPU-free part of the C ABI: configuration validation,
 // capacity / layout / task-count arithmetic, and the seeded synthetic inputs.
 // Each function restates the reference rule it cites; none of it runs on the hot path.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <random>
@@ -142,6 +143,41 @@ fdmoe_status fdmoe_synth_shards(const fdmoe_config* c, uint64_t seed, float* sha
         std::normal_distribution<float> dist(0.0f, 1.0f);
         float* a = shards + d * S * H;
         for (int64_t i = 0; i < S * H; ++i) a[i] = dist(rng);
+    }
+    return FDMOE_OK;
+}
+
+// Straggler hold-back (runtime.hpp:312-326, 341-362): the straggling device draws one delay per
+// (destination, local expert) packet, in that order, from std::mt19937_64(seed ^ 0x9E37...*(dev+1)),
+// each distribution constructed afresh per draw as sample_delay_ms does, and sleeps it before the
+// packet's put. cum_ns[e] (e = destination * E_local + local expert) is the running sum in ns: the
+// earliest time after dispatch start that packet e's signal may be published.
+fdmoe_status fdmoe_straggler_delays(const fdmoe_options* o, int64_t devices, int64_t local_experts,
+                                    uint64_t* cum_ns) {
+    if (!o || !cum_ns) return fail(FDMOE_ERR_CONFIG, "null argument");
+    if (o->straggler_kind < FDMOE_STRAGGLER_NONE || o->straggler_kind > FDMOE_STRAGGLER_LOGNORMAL)
+        return fail(FDMOE_ERR_CONFIG, "unknown straggler kind");
+    if (o->straggler_device < 0 || o->straggler_device >= devices)
+        return fail(FDMOE_ERR_CONFIG, "straggler device outside [0, devices)");
+    std::mt19937_64 rng(o->seed ^ (0x9E3779B97F4A7C15ull * ((uint64_t)o->straggler_device + 1ull)));
+    double cum_ms = 0.0;
+    for (int64_t e = 0; e < devices * local_experts; ++e) {
+        double ms = 0.0;
+        switch (o->straggler_kind) {
+            case FDMOE_STRAGGLER_NONE: break;
+            case FDMOE_STRAGGLER_CONSTANT: ms = o->straggler_a; break;
+            case FDMOE_STRAGGLER_UNIFORM: {
+                std::uniform_real_distribution<double> u(o->straggler_a, o->straggler_b);
+                ms = u(rng);
+                break;
+            }
+            default: {
+                std::lognormal_distribution<double> ln(std::log(std::max(o->straggler_a, 1e-9)), o->straggler_b);
+                ms = ln(rng);
+            }
+        }
+        if (ms > 0.0) cum_ms += ms;
+        cum_ns[e] = (uint64_t)std::llround(cum_ms * 1e6);
     }
     return FDMOE_OK;
 }

@@ -29,6 +29,7 @@ constexpr int kMaxSrcPerTile = 8;   // packet_rows >= 16 -> <= 8 packets per 128
 constexpr int kCombineTok = 16;     // tokens per combine task (== kGateTok)
 constexpr int kMaxLocalRanks = 8;   // ranks per launch (virtual ranks on one GPU)
 constexpr int kTracePts = 20;
+constexpr int kGroupBarriers = 2;   // sequential mode: after dispatch, after the expert FFN
 constexpr int kChunkLog = 512;       // start, gate, barrier, dispatch, gemm, combine, end, tiles,
                                     // then FFN pipeline wait cycles (see kWait*)
 enum WaitSlot : int {
@@ -44,8 +45,18 @@ struct HeapLayout {
     uint64_t yc;          // combine-in rows: [E_total][C][H] fp32
     uint64_t dflag[2];    // [parity] -> [E_local][P] u64 dispatch signals
     uint64_t cflag[2];    // [parity] -> [E_total][RBF][NB1] u64 combine tile signals
+    uint64_t gbar;        // [kGroupBarriers][P] u64 group-barrier arrivals (sequential mode)
     uint64_t bytes;
 };
+
+// One device event record; layout identical to fdmoe_event (include/fdmoe.h).
+struct DevEvent {
+    uint64_t t0, t1;
+    int32_t kind, cta, type, src, expert, rb, cb, peer;
+    int64_t value;
+};
+enum EvKind : int { kEvSpawn = 0, kEvGateDone, kEvDispatchPut, kEvExec, kEvTilePut, kEvBarrierEnter, kEvBarrierExit };
+enum EvTask : int { kTaskGemm0 = 1, kTaskGemm1 = 2, kTaskCombine = 3 };
 
 // Everything one rank's kernel needs. Lives in device global memory (64B aligned
 // so the embedded TMA descriptors are valid operands of cp.async.bulk.tensor).
@@ -84,6 +95,10 @@ struct alignas(64) RankCtx {
     unsigned long long* stats; // [8] gemm0, gemm1, combine tasks, dispatch rows, ...
     unsigned long long* trace; // [ctas][kTracePts] %globaltimer per phase boundary (device trace)
     unsigned long long* chunklog;   // debug: CTA 0 MMA-warp chunk timeline [kChunkLog][4] (null = off)
+    const unsigned long long* delay_ns;   // [E_total] straggler: cumulative hold-back of packet e's signal
+    DevEvent* ev;              // [ev_cap] device event log (fdmoe_event layout)
+    uint32_t* ev_ctr;          // records emitted this launch (reset by the host before the launch)
+    uint32_t ev_cap;
     int32_t rank;
 };
 
@@ -99,7 +114,9 @@ struct LaunchParams {
     unsigned long long launch_seq;   // barrier generation
     unsigned long long budget_ns;    // watchdog budget
     uint32_t* abort_flag;      // per launch-group abort word
-    int sequential;            // bulk-synchronous schedule (grid barrier after each phase)
+    int sequential;            // bulk-synchronous schedule (group barrier after dispatch and after the FFN)
+    int trace_events;          // record the device event log
+    int straggler_rank;        // rank whose packet signals are held back by delay_ns (-1: none)
     int debug;                 // ablation bits (FDMOE_DEBUG env; 0 in production): see kDbg*
     int exact_gate;            // 1: reference-exact logits for every token (bit-exact G_phi, weights)
     float gate_u;              // certified gate: u' = 2^-24 * 1.001

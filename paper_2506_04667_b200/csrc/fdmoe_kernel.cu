@@ -180,6 +180,62 @@ __device__ bool rank_barrier(const LaunchParams& P, const RankCtx& R, unsigned l
     return s_ok != 0;
 }
 
+// Device event log (fdmoe_read_events; the reference's TraceBuffer::emit, trace.hpp:79-96).
+__device__ __forceinline__ void emit_event(const LaunchParams& P, const RankCtx& R, int kind, int cta, int type,
+                                           uint64_t t0, uint64_t t1, int src, int expert, int rb, int cb, int peer,
+                                           long long value) {
+    if (!P.trace_events) return;
+    const uint32_t i = atomicAdd(R.ev_ctr, 1u);
+    if (i >= R.ev_cap) return;
+    DevEvent e;
+    e.t0 = t0; e.t1 = t1; e.kind = kind; e.cta = cta; e.type = type; e.src = src; e.expert = expert;
+    e.rb = rb; e.cb = cb; e.peer = peer; e.value = value;
+    R.ev[i] = e;
+}
+
+// Group barrier over every CTA of every rank (ScheduleMode::sequential's SpinBarrier,
+// runtime.hpp:175-198, 885-908): rank-local barrier, then CTA 0 of each rank publishes an
+// epoch-tagged arrival into every peer's gbar[id][rank] (st.release.sys over NVLink) and waits
+// for all P arrivals in its own heap; a second rank-local barrier releases the rank's CTAs.
+// Arrival words carry the epoch; `>=` tolerates a peer that has already moved to the next launch.
+__device__ bool group_barrier(const LaunchParams& P, const RankCtx& R, unsigned long long gen, int id, int cta) {
+    if (!rank_barrier(P, R, gen)) return false;
+    __shared__ int s_gok;
+    if (threadIdx.x == 0) {
+        s_gok = 1;
+        const uint64_t t0 = globaltimer();
+        if (cta == 0) {
+            emit_event(P, R, kEvBarrierEnter, cta, 0, t0, 0, -1, -1, -1, -1, -1, id);
+            __threadfence_system();
+            for (int q = 0; q < P.P; ++q) {
+                unsigned long long* f =
+                    reinterpret_cast<unsigned long long*>(R.peer_heap[q] + R.hl.gbar) + (size_t)id * P.P + R.rank;
+                st_release_sys(f, ((uint64_t)P.epoch << 32) | 1u);
+            }
+            const unsigned long long* mine =
+                reinterpret_cast<const unsigned long long*>(R.peer_heap[R.rank] + R.hl.gbar) + (size_t)id * P.P;
+            uint32_t n = 0;
+            for (int q = 0; q < P.P && s_gok; ++q) {
+                while ((uint32_t)(ld_acquire_sys(mine + q) >> 32) < P.epoch) {
+                    if ((++n & 255u) == 0) {
+                        if (ld_volatile_u32(P.abort_flag)) { s_gok = 0; break; }
+                        if (globaltimer() - t0 > P.budget_ns) {
+                            raise_error(P, R, kErrTimeout, 110 + id, (uint32_t)q, 0);
+                            s_gok = 0;
+                            break;
+                        }
+                    }
+                }
+            }
+            emit_event(P, R, kEvBarrierExit, cta, 0, globaltimer(), 0, -1, -1, -1, -1, -1, id);
+        }
+    }
+    __syncthreads();
+    const bool ok = s_gok != 0;
+    if (!rank_barrier(P, R, gen + 1)) return false;
+    return ok;
+}
+
 // ================================================================ phase 1: gate
 // Each CTA owns a contiguous, balanced token range (its gate blocks [b0, b1)), processed in
 // sub-tiles of <= gate_sub(Ep) tokens (120 at E <= 128); K streams through a 3-stage cp.async ring
@@ -797,6 +853,17 @@ __device__ void dispatch_phase(const LaunchParams& P, const RankCtx& R, const fl
     int* sKept = sN + kMaxExperts;                 // rows of e kept from this CTA
     const uint32_t par = P.epoch & 1u;
     const uint64_t sig_hi = (uint64_t)P.epoch << 32;
+    const uint64_t t_disp0 = globaltimer();
+    const bool straggle = P.straggler_rank == R.rank;
+    // straggler (runtime.hpp:358-362): packet e's signal is held back until its cumulative delay
+    auto hold = [&](int e) {
+        if (!straggle) return;
+        const uint64_t until = t_disp0 + R.delay_ns[e];
+        while (globaltimer() < until) {
+            if (ld_volatile_u32(P.abort_flag)) return;
+            __nanosleep(1000);
+        }
+    };
 
     for (int e = tid; e < E; e += kThreads) {
         int base = 0, tot = 0;
@@ -820,7 +887,9 @@ __device__ void dispatch_phase(const LaunchParams& P, const RankCtx& R, const fl
                 const int q = e / P.El, le = e % P.El;
                 unsigned long long* f = reinterpret_cast<unsigned long long*>(R.peer_heap[q] + R.hl.dflag[par]) +
                                         (size_t)le * P.P + R.rank;
+                hold(e);
                 st_release_sys(f, sig_hi);
+                emit_event(P, R, kEvDispatchPut, cta, 0, globaltimer(), 0, R.rank, le, -1, -1, q, 0);
             }
         }
     }
@@ -929,7 +998,9 @@ __device__ void dispatch_phase(const LaunchParams& P, const RankCtx& R, const fl
             const int q = e / P.El, le = e % P.El;
             unsigned long long* f =
                 reinterpret_cast<unsigned long long*>(R.peer_heap[q] + R.hl.dflag[par]) + (size_t)le * P.P + R.rank;
+            hold(e);
             st_release_sys(f, sig_hi | (uint32_t)sN[e]);
+            emit_event(P, R, kEvDispatchPut, cta, 0, globaltimer(), 0, R.rank, le, -1, -1, q, sN[e]);
         } else if ((int)(old + kept) > sN[e]) {
             raise_error(P, R, kErrProtocol, 200, e, old + kept);
         }
@@ -950,6 +1021,7 @@ struct Task {
     int le, nb, m;
     int nsrc, src0;
     int cnt[kMaxSrcPerTile];   // valid rows per packet in the tile
+    uint64_t t0;               // event log: dependencies resolved, operand streaming starts
 };
 
 // Stage = BK elements of K = NATOM SWIZZLE_128B atoms (128-byte rows). One wait + one commit per
@@ -1099,6 +1171,7 @@ __device__ void gemm_producer(const LaunchParams& P, const RankCtx& R, uint8_t* 
             trace[kProdFetch] = t_fetch;
             return;
         }
+        tk.t0 = P.trace_events ? globaltimer() : 0;
         G.ring[q] = tk;
         mbar_arrive(&G.qfull[q]);
         if (++q == kTaskRing) { q = 0; qphase ^= 1u; }
@@ -1424,18 +1497,28 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
         asm volatile("bar.sync 1, 128;" ::: "memory");   // all rows stored, TMEM drained
         if (et == 0) {
             mbar_arrive(&G.tempty[acc]);
+            int rows = 0;
+            for (int j = 0; j < tk.nsrc; ++j) rows += tk.cnt[j];
             if (type == 0) {
                 __threadfence();
+                // event before the counter release: GEMM0's end precedes any dependent GEMM1 start
+                emit_event(P, R, kEvExec, blockIdx.x % P.ctas_per_rank, kTaskGemm0, tk.t0, globaltimer(), tk.src0,
+                           tk.le, tk.m, tk.nb, tk.nsrc, rows);
                 atomicAdd(R.g0done + (size_t)tk.le * P.MT + tk.m, 1u);
                 stat[0]++;
             } else {
                 __threadfence_system();
+                const int cta = blockIdx.x % P.ctas_per_rank;
+                emit_event(P, R, kEvExec, cta, kTaskGemm1, tk.t0, globaltimer(), tk.src0, tk.le, tk.m, tk.nb,
+                           tk.nsrc, rows);
                 const int rbf = P.Cp >= kBM ? (tk.m % (P.Cp / kBM)) : 0;
                 for (int j = 0; j < tk.nsrc; ++j) {
                     if (tk.cnt[j] <= 0) continue;
                     unsigned long long* f = reinterpret_cast<unsigned long long*>(R.peer_heap[tk.src0 + j] +
                                                                                   R.hl.cflag[par]) +
                                             ((size_t)e_glob * P.RBF + rbf) * P.NB1 + tk.nb;
+                    emit_event(P, R, kEvTilePut, cta, kTaskGemm1, globaltimer(), 0, R.rank, tk.le, tk.m, tk.nb,
+                               tk.src0 + j, tk.cnt[j]);
                     st_release_sys(f, ((uint64_t)P.epoch << 32) | (uint32_t)tk.cnt[j]);
                 }
                 stat[1]++;
@@ -1479,13 +1562,21 @@ __device__ void combine_phase(const LaunchParams& P, const RankCtx& R, float* __
     if (!__syncthreads_and(ok)) return;
 
     const int H4 = H >> 2;
+    const int cta = blockIdx.x % P.ctas_per_rank;
+    int prev_t = -1;
+    uint64_t prev_t0 = 0;
     while (true) {
         __syncthreads();
         if (tid == 0) {
+            if (prev_t >= 0)
+                emit_event(P, R, kEvExec, cta, kTaskCombine, prev_t0, globaltimer(), R.rank, -1, prev_t, -1, -1,
+                           min(kCombineTok, S - prev_t * kCombineTok));
             int t = ld_volatile_u32(P.abort_flag) ? ntask : (int)atomicAdd(R.comb_head, 1u);
             // routing of these tokens was written by the CTA that gated them (dispatch phase)
             if (t < ntask && !wait_counter_eq(P, R, R.blk_ready + t, P.epoch, 401)) t = ntask;
             sTask[0] = t;
+            prev_t = t < ntask ? t : -1;
+            prev_t0 = P.trace_events ? globaltimer() : 0;
         }
         __syncthreads();
         const int t = sTask[0];
@@ -1585,7 +1676,10 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
 
     // phase 1: exact gate (uses the smem region as scratch)
     gate_phase(P, R, A, cta, smem, s_stat);
-    if (tid == 0) trace[1] = globaltimer();
+    if (tid == 0) {
+        trace[1] = globaltimer();
+        emit_event(P, R, kEvGateDone, cta, 0, trace[0], trace[1], R.rank, -1, -1, -1, -1, 0);
+    }
     if (!rank_barrier(P, R, P.launch_seq)) goto done;
     if (tid == 0) trace[2] = globaltimer();
 
@@ -1593,6 +1687,8 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
     dispatch_phase(P, R, A, cta, smem);
     __syncthreads();
     for (int e = tid; e < P.E; e += kThreads) s_n_expert[e] = reinterpret_cast<const int*>(smem)[kMaxExperts + e];
+    // sequential schedule: every rank's dispatch lands before any expert tile starts
+    if (P.sequential && !group_barrier(P, R, P.launch_seq + 1, 0, cta)) goto done;
     if (tid == 0) trace[3] = globaltimer();
 
     // phase 3: expert FFN tiles
@@ -1618,6 +1714,8 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
         gemm_epilogue<PREC>(P, R, G, s_stat, trace);
     }
     __syncthreads();
+    // sequential schedule: every rank's expert compute drains before any combine starts
+    if (P.sequential && !group_barrier(P, R, P.launch_seq + 3, 1, cta)) goto done;
     if (tid == 0) trace[4] = globaltimer();
 
     // phase 4: combine
@@ -1629,6 +1727,7 @@ done:
     if (tid == 0) {
         trace[6] = globaltimer();
         trace[7] = s_stat[0] + s_stat[1];
+        emit_event(P, R, kEvSpawn, cta, 0, trace[0], trace[6], R.rank, -1, -1, -1, -1, 0);
     }
     if (warp == kWarpTmem) {
         tc_fence_after();

@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <random>
 #include <string>
 #include <vector>
 
@@ -114,6 +115,9 @@ struct RankRes {
     uint32_t* blk_ready = nullptr;
     unsigned long long* trace = nullptr;
     unsigned long long* chunklog = nullptr;
+    unsigned long long* delay_ns = nullptr;
+    DevEvent* ev = nullptr;
+    uint32_t ev_cap = 0;
     int ctas = 0;
     uint8_t* ctrl = nullptr;        // bar | heads | err | stats | sent | g0done
     float* in_buf = nullptr;
@@ -156,6 +160,15 @@ struct fdmoe_handle {
 namespace {
 
 size_t ctrl_bytes(const Dims& d) { return align_up(kCtrlSent + 4 * d.E + 4 * d.El * d.MT + 64, 256); }
+size_t ctrl_ev_ctr(const Dims& d) { return kCtrlSent + 4 * d.E + 4 * d.El * d.MT; }
+
+// Event-log capacity: every task, tile put, packet signal, per-CTA record and barrier of one launch.
+uint32_t event_capacity(const Dims& d, int ctas) {
+    const int64_t tiles = d.El * d.MT;
+    const int64_t n = tiles * (d.NB0 + d.NB1) + tiles * d.NB1 * std::min<int64_t>(d.P, kMaxSrcPerTile) +
+                      (d.S + kCombineTok - 1) / kCombineTok + d.E + 2 * (int64_t)ctas + 4 * kGroupBarriers + 1024;
+    return (uint32_t)std::min<int64_t>(n, 1 << 26);
+}
 
 fdmoe_status alloc_rank(fdmoe_handle* h, RankRes& r, int ctas_per_rank) {
     const Dims& d = h->dm;
@@ -172,6 +185,7 @@ fdmoe_status alloc_rank(fdmoe_handle* h, RankRes& r, int ctas_per_rank) {
     hl.yc = off; off += align_up((size_t)d.E * d.C * d.H * 4);
     for (int par = 0; par < 2; ++par) { hl.dflag[par] = off; off += align_up((size_t)d.El * d.P * 8); }
     for (int par = 0; par < 2; ++par) { hl.cflag[par] = off; off += align_up((size_t)d.E * d.RBF * d.NB1 * 8); }
+    hl.gbar = off; off += align_up((size_t)kGroupBarriers * d.P * 8);
     hl.bytes = off;
     r.hl = hl;
     r.heap_bytes = off;
@@ -202,6 +216,9 @@ fdmoe_status alloc_rank(fdmoe_handle* h, RankRes& r, int ctas_per_rank) {
     parts.push_back({(void**)&r.slot_counts, (size_t)d.E * 4});
     parts.push_back({(void**)&r.trace, (size_t)ctas_per_rank * kTracePts * 8});
     parts.push_back({(void**)&r.chunklog, (size_t)kChunkLog * 4 * 8});
+    parts.push_back({(void**)&r.delay_ns, (size_t)d.E * 8});
+    r.ev_cap = event_capacity(d, ctas_per_rank);
+    parts.push_back({(void**)&r.ev, (size_t)r.ev_cap * sizeof(DevEvent)});
     parts.push_back({(void**)&r.blk_ready, (size_t)(d.S + kGateTok - 1) / kGateTok * 4});
     parts.push_back({(void**)&r.ctrl, ctrl_bytes(d)});
     parts.push_back({(void**)&r.in_buf, (size_t)d.S * d.H * 4});
@@ -215,6 +232,7 @@ fdmoe_status alloc_rank(fdmoe_handle* h, RankRes& r, int ctas_per_rank) {
     r.ctas = ctas_per_rank;
     CK(cudaMemset(r.trace, 0, (size_t)ctas_per_rank * kTracePts * 8));
     CK(cudaMemset(r.ctrl, 0, ctrl_bytes(d)));
+    CK(cudaMemset(r.delay_ns, 0, (size_t)d.E * 8));
     CK(cudaMemset(r.blk_ready, 0, (size_t)(d.S + kGateTok - 1) / kGateTok * 4));
     CK(cudaMemset(r.w1[0], 0, w1plane));   // padding rows stay finite
     CK(cudaMemset(r.w2[0], 0, w2plane));
@@ -251,6 +269,10 @@ fdmoe_status build_ctx(fdmoe_handle* h) {
             c.blk_ready = r.blk_ready;
             c.trace = r.trace;
             c.chunklog = getenv("FDMOE_CHUNKLOG") ? r.chunklog : nullptr;
+            c.delay_ns = r.delay_ns;
+            c.ev = r.ev;
+            c.ev_cap = r.ev_cap;
+            c.ev_ctr = reinterpret_cast<uint32_t*>(r.ctrl + ctrl_ev_ctr(d));
             c.bar = reinterpret_cast<unsigned long long*>(r.ctrl + kCtrlBar);
             c.gemm_head = reinterpret_cast<uint32_t*>(r.ctrl + kCtrlGemm);
             c.comb_head = reinterpret_cast<uint32_t*>(r.ctrl + kCtrlComb);
@@ -496,9 +518,21 @@ static fdmoe_status launch_all(fdmoe_handle* h, const float* const* in_dev, floa
     const Dims& d = h->dm;
     if (!h->weights_set) return fail(FDMOE_ERR_CONFIG, "weights not set");
     if (!h->peers_ready) return fail(FDMOE_ERR_CONFIG, "peers not attached (fdmoe_import_peers)");
-    if (opts && opts->sequential)
-        return fail(FDMOE_ERR_UNSUPPORTED, "ScheduleMode::sequential is not implemented on the GPU path yet");
     const int64_t budget_ms = (opts && opts->deadlock_budget_ms > 0) ? opts->deadlock_budget_ms : 5000;
+    const bool sequential = opts && opts->sequential;
+    const bool trace_events = opts && opts->trace_events;
+    int straggler_rank = -1;
+    std::vector<uint64_t> delay;
+    if (opts && opts->straggler_kind != FDMOE_STRAGGLER_NONE) {
+        if (opts->straggler_kind < 0 || opts->straggler_kind > FDMOE_STRAGGLER_LOGNORMAL)
+            return fail(FDMOE_ERR_CONFIG, "unknown straggler kind");
+        if (opts->straggler_device < 0 || opts->straggler_device >= d.P)
+            return fail(FDMOE_ERR_CONFIG, "straggler device outside [0, devices)");
+        straggler_rank = opts->straggler_device;
+        delay.resize(d.E);
+        fdmoe_status ds = fdmoe_straggler_delays(opts, d.P, d.El, delay.data());
+        if (ds) return ds;
+    }
     h->epoch += 1;
     for (auto& g : h->groups) {
         LaunchParams p{};
@@ -518,7 +552,9 @@ static fdmoe_status launch_all(fdmoe_handle* h, const float* const* in_dev, floa
         p.launch_seq = g.launch_seq;
         p.budget_ns = (unsigned long long)budget_ms * 1000000ull;
         p.abort_flag = g.d_abort;
-        p.sequential = 0;
+        p.sequential = sequential ? 1 : 0;
+        p.trace_events = trace_events ? 1 : 0;
+        p.straggler_rank = straggler_rank;
         p.exact_gate = (opts && opts->exact_gate) ? 1 : 0;
         {   // certified-gate bound coefficients (fdmoe_kernel.cu, phase 1)
             const double u = std::ldexp(1.0, -24), n1 = (double)d.H + 1.0;
@@ -530,10 +566,16 @@ static fdmoe_status launch_all(fdmoe_handle* h, const float* const* in_dev, floa
         CK(cudaSetDevice(g.dev));
         cudaStream_t s = g.stream;
         if (streams && streams[g.members[0]]) s = static_cast<cudaStream_t>(streams[g.members[0]]);
+        for (int idx : g.members) {
+            RankRes& r = h->ranks[idx];
+            if (trace_events) CK(cudaMemsetAsync(r.ctrl + ctrl_ev_ctr(d), 0, 4, s));
+            if (r.rank == straggler_rank)
+                CK(cudaMemcpyAsync(r.delay_ns, delay.data(), (size_t)d.E * 8, cudaMemcpyHostToDevice, s));
+        }
         CK(cudaEventRecord(g.ev0, s));
         CK(launch_layer(p, g.ctas_per_rank * (int)g.members.size(), g.smem, s));
         CK(cudaEventRecord(g.ev1, s));
-        g.launch_seq += 1;
+        g.launch_seq += sequential ? 1 + 2 * kGroupBarriers : 1;   // rank-barrier generations used
     }
     h->in_flight = true;
     return FDMOE_OK;
@@ -675,6 +717,23 @@ fdmoe_status fdmoe_read_trace(fdmoe_handle* h, int32_t local_rank, uint64_t* out
     CK(cudaMemcpy(out, r.trace, (size_t)n * kTracePts * 8, cudaMemcpyDeviceToHost));
     CK(cudaMemset(r.trace, 0, (size_t)r.ctas * kTracePts * 8));
     if (n_ctas) *n_ctas = r.ctas;
+    return FDMOE_OK;
+}
+
+fdmoe_status fdmoe_read_events(fdmoe_handle* h, int32_t local_rank, fdmoe_event* out, int64_t cap, int64_t* n,
+                               int64_t* dropped) {
+    static_assert(sizeof(fdmoe_event) == sizeof(DevEvent), "event record layout");
+    if (!h || local_rank < 0 || local_rank >= h->n_local) return fail(FDMOE_ERR_CONFIG, "bad rank");
+    RankRes& r = h->ranks[local_rank];
+    CK(cudaSetDevice(r.dev));
+    for (auto& g : h->groups) if (g.dev == r.dev) CK(cudaEventSynchronize(g.ev1));
+    uint32_t cnt = 0;
+    CK(cudaMemcpy(&cnt, r.ctrl + ctrl_ev_ctr(h->dm), 4, cudaMemcpyDeviceToHost));
+    const int64_t have = std::min<int64_t>(cnt, r.ev_cap);
+    const int64_t k = out ? std::min<int64_t>(have, cap) : 0;
+    if (k > 0) CK(cudaMemcpy(out, r.ev, (size_t)k * sizeof(DevEvent), cudaMemcpyDeviceToHost));
+    if (n) *n = have;
+    if (dropped) *dropped = (int64_t)cnt - have;
     return FDMOE_OK;
 }
 
