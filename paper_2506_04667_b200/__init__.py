@@ -133,8 +133,8 @@ def lib():
     global _LIB
     if _LIB is not None:
         return _LIB
-    path = _build.LIB
-    if not os.path.exists(path) or _build._stale():
+    path = os.environ.get("FDMOE_LIB_OVERRIDE") or _build.LIB   # A/B experiments (tools/); unset in production
+    if path == _build.LIB and (not os.path.exists(path) or _build._stale()):
         try:
             _build.build()
         except Exception as e:  # no nvcc on a deployment box: the prebuilt .so must exist

@@ -124,7 +124,6 @@ struct LaunchParams {
 };
 enum DebugBits : int {
     kDbgNoConvert = 1,    // converter warps skip the split + tcgen05.st (MMA reads stale TMEM)
-    kDbgOneProduct = 2,   // issue only the hi*hi product
     kDbgNoEpiStore = 4,   // epilogue skips global stores
     kDbgNoXTma = 8,       // producer skips the token TMA (barrier completes without data)
     kDbgNoWTma = 16,      // producer skips the weight TMA
@@ -201,6 +200,17 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
         : "r"(smem_u32(bar)), "r"(parity)

@@ -12,8 +12,8 @@ cfg = fd.MoeConfig(tokens_per_device=S, embed_dim=2048, ffn_dim=2048, experts_to
 op = fd.Operator(cfg); op.set_weights(fd.make_model(cfg))
 x = torch.from_numpy(fd.make_shards(cfg)[0]).cuda(); y = torch.empty_like(x)
 st = torch.cuda.Stream(); torch.cuda.set_stream(st)
-names = {0: "baseline", 1: "no convert/STTM", 2: "1 product", 3: "no convert + 1 product", 4: "no epilogue stores",
-         8: "no token TMA", 16: "no weight TMA", 24: "no TMA at all", 7: "no conv+1prod+no epi", 31: "all off"}
+names = {0: "baseline", 1: "no convert/STTM", 4: "no epilogue stores",
+         8: "no token TMA", 16: "no weight TMA", 24: "no TMA at all", 5: "no conv + no epi", 29: "all off"}
 for d, n in names.items():
     os.environ["FDMOE_DEBUG"] = str(d)
     for _ in range(3):
