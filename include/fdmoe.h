@@ -201,6 +201,13 @@ fdmoe_status fdmoe_forward(fdmoe_handle* h, const float* const* in_shards, float
  * one per local rank; NULL = the handle's own stream). Pair with fdmoe_sync. */
 fdmoe_status fdmoe_forward_async(fdmoe_handle* h, const float* const* in_dev, float* const* out_dev,
                                  void* const* streams, const fdmoe_options* opts);
+/* Serving loop over n_batches host batches (in_batches / out_batches: n_batches * n_local host
+ * pointers, batch-major; pinned memory for overlap). Batch b's host->device copy, layer launch and
+ * device->host copy run on three streams with double-buffered device shards, so the PCIe copies of
+ * neighbouring batches overlap the launch of batch b. One kernel launch per device per batch;
+ * synchronous (returns when every output has landed). */
+fdmoe_status fdmoe_forward_stream(fdmoe_handle* h, int32_t n_batches, const float* const* in_batches,
+                                  float* const* out_batches, const fdmoe_options* opts);
 /* Wait for the last forward, check the device watchdog/error word. */
 fdmoe_status fdmoe_sync(fdmoe_handle* h);
 

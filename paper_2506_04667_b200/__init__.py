@@ -122,7 +122,7 @@ EXPORTED_SYMBOLS = [
     "fdmoe_synth_model", "fdmoe_synth_shards", "fdmoe_create", "fdmoe_destroy", "fdmoe_ipc_size",
     "fdmoe_export_heap", "fdmoe_import_peers", "fdmoe_set_weights", "fdmoe_forward", "fdmoe_forward_async",
     "fdmoe_sync", "fdmoe_get_info", "fdmoe_last_kernel_ms", "fdmoe_read_trace", "fdmoe_debug_expf", "fdmoe_debug_gemm", "fdmoe_debug_mma_rate", "fdmoe_debug_latency", "fdmoe_read_chunklog",
-    "fdmoe_read_events", "fdmoe_straggler_delays",
+    "fdmoe_read_events", "fdmoe_straggler_delays", "fdmoe_forward_stream",
 ]
 
 _LIB = None
@@ -175,6 +175,7 @@ def lib():
         "fdmoe_read_chunklog": (i32, [vp, vp]),
         "fdmoe_read_events": (i32, [vp, i32, vp, i64, vp, vp]),
         "fdmoe_straggler_delays": (i32, [C.POINTER(_Opts), i64, i64, vp]),
+        "fdmoe_forward_stream": (i32, [vp, i32, vp, vp, C.POINTER(_Opts)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -569,6 +570,24 @@ class Operator:
         sp = (C.c_void_p * n)(*(streams or [0] * n))
         copts = (opts or ForwardOptions()).to_c()
         _check(lib().fdmoe_forward_async(self._h, ip, op, sp, C.byref(copts)))
+
+    def forward_stream(self, batches: Sequence[Sequence[np.ndarray]], outs: Sequence[Sequence[np.ndarray]],
+                       opts: Optional[ForwardOptions] = None):
+        """Serving loop over host batches (each a list of n_local S x H FP32 arrays, ideally pinned):
+        copies of neighbouring batches overlap each launch (fdmoe_forward_stream)."""
+        n = self.n_local
+        S, H = self.cfg.tokens_per_device, self.cfg.embed_dim
+        ins = [a for b in batches for a in b]
+        os_ = [a for b in outs for a in b]
+        if len(ins) != len(batches) * n or len(os_) != len(ins):
+            raise ConfigError("forward_stream: every batch needs n_local input and output shards")
+        for a in ins + os_:
+            if a.shape != (S, H) or a.dtype != np.float32 or not a.flags["C_CONTIGUOUS"]:
+                raise ConfigError("forward_stream: shards must be contiguous S x H float32")
+        ip = (C.c_void_p * len(ins))(*[a.ctypes.data for a in ins])
+        op_ = (C.c_void_p * len(os_))(*[a.ctypes.data for a in os_])
+        copts = (opts or ForwardOptions()).to_c()
+        _check(lib().fdmoe_forward_stream(self._h, len(batches), ip, op_, C.byref(copts)))
 
     def sync(self):
         _check(lib().fdmoe_sync(self._h))

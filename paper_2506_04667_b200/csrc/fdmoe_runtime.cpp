@@ -122,6 +122,8 @@ struct RankRes {
     uint8_t* ctrl = nullptr;        // bar | heads | err | stats | sent | g0done
     float* in_buf = nullptr;
     float* out_buf = nullptr;
+    float* in_buf2 = nullptr;       // second shard buffers of the streaming API (allocated on first use)
+    float* out_buf2 = nullptr;
     size_t weight_bytes = 0;
     std::vector<uint8_t*> peer;     // heap of every rank as addressable from this rank's device
     std::vector<bool> peer_opened;  // opened through IPC (must be closed)
@@ -134,6 +136,9 @@ struct Group {
     uint32_t* d_abort = nullptr;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // streaming API (fdmoe_forward_stream): copy-in / copy-out streams and per-slot events
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
     int ctas_per_rank = 0;
     int smem = 0;
     int num_sms = 0;
@@ -412,12 +417,21 @@ fdmoe_status fdmoe_destroy(fdmoe_handle* h) {
             if (r.peer_opened[q]) cudaIpcCloseMemHandle(r.peer[q]);
         if (r.heap) cudaFree(r.heap);
         if (r.scratch) cudaFree(r.scratch);
+        if (r.in_buf2) cudaFree(r.in_buf2);
+        if (r.out_buf2) cudaFree(r.out_buf2);
     }
     for (auto& g : h->groups) {
         cudaSetDevice(g.dev);
         if (g.stream) cudaStreamDestroy(g.stream);
         if (g.ev0) cudaEventDestroy(g.ev0);
         if (g.ev1) cudaEventDestroy(g.ev1);
+        if (g.s_in) cudaStreamDestroy(g.s_in);
+        if (g.s_out) cudaStreamDestroy(g.s_out);
+        for (int i = 0; i < 2; ++i) {
+            if (g.ev_in[i]) cudaEventDestroy(g.ev_in[i]);
+            if (g.ev_comp[i]) cudaEventDestroy(g.ev_comp[i]);
+            if (g.ev_out[i]) cudaEventDestroy(g.ev_out[i]);
+        }
         if (g.d_ctx) cudaFree(g.d_ctx);
         if (g.d_abort) cudaFree(g.d_abort);
     }
@@ -691,6 +705,75 @@ fdmoe_status fdmoe_forward(fdmoe_handle* h, const float* const* in_shards, float
         }
     }
     return FDMOE_OK;
+}
+
+// Serving loop over host batches: batch b's H2D (stream s_in), layer launch (the group stream) and
+// D2H (stream s_out) run on three streams with double-buffered device shards, so the PCIe copies of
+// batches b-1 and b+1 overlap the launch of batch b (H2D and D2H overlap each other: PCIe is full
+// duplex). Still exactly one kernel launch per device per batch.
+fdmoe_status fdmoe_forward_stream(fdmoe_handle* h, int32_t n_batches, const float* const* in_batches,
+                                  float* const* out_batches, const fdmoe_options* opts) {
+    if (!h || !in_batches || !out_batches || n_batches < 1) return fail(FDMOE_ERR_CONFIG, "null argument");
+    const Dims& d = h->dm;
+    const size_t shard_bytes = (size_t)d.S * d.H * 4;
+    for (auto& g : h->groups) {
+        CK(cudaSetDevice(g.dev));
+        if (!g.s_in) {
+            CK(cudaStreamCreateWithFlags(&g.s_in, cudaStreamNonBlocking));
+            CK(cudaStreamCreateWithFlags(&g.s_out, cudaStreamNonBlocking));
+            for (int i = 0; i < 2; ++i) {
+                CK(cudaEventCreateWithFlags(&g.ev_in[i], cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&g.ev_comp[i], cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&g.ev_out[i], cudaEventDisableTiming));
+            }
+        }
+        for (int idx : g.members) {
+            RankRes& r = h->ranks[idx];
+            if (!r.in_buf2) CK(cudaMalloc(&r.in_buf2, shard_bytes));
+            if (!r.out_buf2) CK(cudaMalloc(&r.out_buf2, shard_bytes));
+        }
+    }
+    const int n = h->n_local;
+    std::vector<const float*> din(n);
+    std::vector<float*> dout(n);
+    for (int b = 0; b < n_batches; ++b) {
+        const int slot = b & 1;
+        for (auto& g : h->groups) {
+            CK(cudaSetDevice(g.dev));
+            if (b >= 2) CK(cudaStreamWaitEvent(g.s_in, g.ev_comp[slot], 0));   // launch b-2 done with the slot
+            for (int idx : g.members) {
+                RankRes& r = h->ranks[idx];
+                CK(cudaMemcpyAsync(slot ? r.in_buf2 : r.in_buf, in_batches[(size_t)b * n + idx], shard_bytes,
+                                   cudaMemcpyHostToDevice, g.s_in));
+            }
+            CK(cudaEventRecord(g.ev_in[slot], g.s_in));
+            CK(cudaStreamWaitEvent(g.stream, g.ev_in[slot], 0));
+            if (b >= 2) CK(cudaStreamWaitEvent(g.stream, g.ev_out[slot], 0));   // D2H of b-2 drained the slot
+        }
+        for (int i = 0; i < n; ++i) {
+            din[i] = slot ? h->ranks[i].in_buf2 : h->ranks[i].in_buf;
+            dout[i] = slot ? h->ranks[i].out_buf2 : h->ranks[i].out_buf;
+        }
+        fdmoe_status st = launch_all(h, din.data(), dout.data(), nullptr, opts);
+        if (st) return st;
+        for (auto& g : h->groups) {
+            CK(cudaSetDevice(g.dev));
+            CK(cudaEventRecord(g.ev_comp[slot], g.stream));
+            CK(cudaStreamWaitEvent(g.s_out, g.ev_comp[slot], 0));
+            for (int idx : g.members) {
+                RankRes& r = h->ranks[idx];
+                CK(cudaMemcpyAsync(out_batches[(size_t)b * n + idx], slot ? r.out_buf2 : r.out_buf, shard_bytes,
+                                   cudaMemcpyDeviceToHost, g.s_out));
+            }
+            CK(cudaEventRecord(g.ev_out[slot], g.s_out));
+        }
+    }
+    for (auto& g : h->groups) {
+        CK(cudaSetDevice(g.dev));
+        CK(cudaStreamSynchronize(g.s_out));
+    }
+    h->in_flight = false;
+    return check_errors(h);
 }
 
 fdmoe_status fdmoe_get_info(fdmoe_handle* h, fdmoe_info* info) {

@@ -113,3 +113,22 @@ def test_lognormal_straggler_sequential_slower_than_overlapped():
     assert sq_ms >= ov_ms * 0.9
     for d in range(4):
         assert np.array_equal(sq.outputs[d].view(np.uint32), ov.outputs[d].view(np.uint32))
+
+
+def test_forward_stream_matches_single_launches():
+    """fdmoe_forward_stream (copies of neighbouring batches overlapping each launch) computes exactly
+    what one synchronous forward per batch computes."""
+    import torch
+    cfg = _cfg(2, 8, S=256)
+    model = fd.make_model(cfg)
+    op = fd.Operator(cfg)
+    op.set_weights(model)
+    batches = [fd.make_shards(cfg, seed=200 + b) for b in range(5)]
+    pin = [[torch.from_numpy(a.copy()).pin_memory().numpy() for a in b] for b in batches]
+    outs = [[torch.empty(a.shape, dtype=torch.float32).pin_memory().numpy() for a in b] for b in batches]
+    op.forward_stream(pin, outs)
+    for b, shards in enumerate(batches):
+        want = op.forward(shards, routing=False, stats=False).outputs
+        for d in range(2):
+            assert np.array_equal(outs[b][d].view(np.uint32), want[d].view(np.uint32)), (b, d)
+    op.close()
