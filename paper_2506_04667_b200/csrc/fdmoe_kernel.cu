@@ -1388,6 +1388,7 @@ __device__ void gemm_mma(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, unsi
         long long t_rdy = chunklog ? clk() : 0;
         if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.ready[stage], phase, P.abort_flag))) return;
         tc_fence_after();
+#pragma unroll 4   // fewer loop back-edges (and their YIELDs) between stages: measured best of 1/4/8/16
         for (int kb = 0; kb < nk; ++kb) {
             const long long t_iss = chunklog ? clk() : 0;
             const uint32_t abase = tmem + Cfg::TMEM_A0 + stage * Cfg::A_COLS;
