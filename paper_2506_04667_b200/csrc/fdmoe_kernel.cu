@@ -850,7 +850,6 @@ __device__ void dispatch_phase(const LaunchParams& P, const RankCtx& R, const fl
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int* sRun = reinterpret_cast<int*>(smem);     // running slot counter per expert
     int* sN = sRun + kMaxExperts;                  // n_e = min(total, C)
-    int* sKept = sN + kMaxExperts;                 // rows of e kept from this CTA
     const uint32_t par = P.epoch & 1u;
     const uint64_t sig_hi = (uint64_t)P.epoch << 32;
     const uint64_t t_disp0 = globaltimer();
@@ -867,16 +866,21 @@ __device__ void dispatch_phase(const LaunchParams& P, const RankCtx& R, const fl
 
     for (int e = tid; e < E; e += kThreads) {
         int base = 0, tot = 0;
-        for (int c = 0; c < P.ctas_per_rank; ++c) {
-            const int v = R.cnt_cta[(size_t)c * E + e];
-            if (c < cta) base += v;
-            tot += v;
+        // per-CTA pick counts of expert e (coalesced across threads); 8 loads in flight per batch —
+        // a plain loop pays one L2 round trip per CTA (148 in a row: ~40 us)
+        for (int c0 = 0; c0 < P.ctas_per_rank; c0 += 8) {
+            int v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = c0 + u < P.ctas_per_rank ? __ldcg(R.cnt_cta + (size_t)(c0 + u) * E + e) : 0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (c0 + u < cta) base += v[u];
+                tot += v[u];
+            }
         }
-        const int mine = R.cnt_cta[(size_t)cta * E + e];
         const int n = min(tot, C);
         sRun[e] = base;
         sN[e] = n;
-        sKept[e] = max(0, min(C - base, mine));
         if (cta == 0) {
             R.slot_counts[e] = n;
             for (int s = n; s < C; ++s) {
@@ -894,103 +898,175 @@ __device__ void dispatch_phase(const LaunchParams& P, const RankCtx& R, const fl
         }
     }
     __syncthreads();
+    if (tid == 0) R.trace[(size_t)cta * kTracePts + kTrPrefix] = globaltimer();
 
     int tokA, tokB, b0, b1;
     gate_token_range(P, cta, tokA, tokB, b0, b1);
 
-    // slot assignment in ascending token order (one warp, lane = token in block):
-    // slot = (picks of e by earlier CTAs) + (by earlier blocks of this CTA) + (by earlier
-    // tokens of this block) -- exactly the sequential counter of gate.hpp:94-103.
-    if (warp == 0) {
-        for (int blk = b0; blk < b1; ++blk) {
-            const int tok = blk * kGateTok + lane;
-            const bool valid = lane < kGateTok && tok < S;
-            int mye[8];
+    // slot assignment in ascending token order: slot = (picks of e by earlier CTAs) + (by earlier
+    // blocks of this CTA) + (by earlier tokens of this block) -- exactly the sequential counter of
+    // gate.hpp:94-103. Blocks go 12 at a time, one warp each: (A) per-block pick counts per expert,
+    // (B) exclusive prefix over the group's blocks on top of the running counter, (C) each warp ranks
+    // its block's picks (lane = token) and writes slots / T_phi.
+    int* sGrp = sRun + 8 * kMaxExperts;   // [kWarps][E] pick counts of the group's blocks
+    constexpr int kWarps = kThreads / 32;
+    for (int g0 = b0; g0 < b1; g0 += kWarps) {
+        const int blk = g0 + warp;
+        const bool wv = blk < b1;
+        const int tok = blk * kGateTok + lane;
+        const bool valid = wv && lane < kGateTok && tok < S;
+        for (int i = tid; i < kWarps * E; i += kThreads) sGrp[i] = 0;
+        __syncthreads();
+        int mye[8];
+        float myw[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) mye[j] = (valid && j < K) ? R.pick_e[(size_t)tok * K + j] : -1;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                if (j >= K) break;
-                const int e = mye[j];
-                int rank = 0;
-                for (int t2 = 0; t2 < 32; ++t2) {
-#pragma unroll
-                    for (int j2 = 0; j2 < 8; ++j2) {
-                        if (j2 >= K) break;
-                        const int e2 = __shfl_sync(0xffffffffu, mye[j2], t2);
-                        if (t2 < lane && e2 == e) ++rank;
-                    }
-                }
-                if (valid) {
-                    const int slot = sRun[e] + rank;
-                    if (slot < C) {
-                        R.pick_slot[(size_t)tok * K + j] = slot;
-                        R.tbl_tok[(size_t)e * C + slot] = tok;
-                        R.tbl_w[(size_t)e * C + slot] = R.pick_w[(size_t)tok * K + j];
-                    } else {
-                        R.pick_slot[(size_t)tok * K + j] = -1;
-                    }
-                }
-            }
-            __syncwarp();
-            if (valid) {
-#pragma unroll
-                for (int j = 0; j < 8; ++j)
-                    if (j < K) atomicAdd(&sRun[mye[j]], 1);
-            }
-            __syncwarp();
-            // this block's picks/slots/weights are final: the combine (any CTA) acquires this
-            __threadfence();
-            if (lane == 0) st_release_gpu_u32(R.blk_ready + blk, P.epoch);
+        for (int j = 0; j < 8; ++j) {
+            mye[j] = (valid && j < K) ? R.pick_e[(size_t)tok * K + j] : -1;
+            myw[j] = (valid && j < K) ? R.pick_w[(size_t)tok * K + j] : 0.0f;
         }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (j < K && valid) atomicAdd(&sGrp[warp * E + mye[j]], 1);
+        __syncthreads();
+        for (int e = tid; e < E; e += kThreads) {   // (B): counts -> bases, running counter advances
+            int run = sRun[e];
+            for (int w = 0; w < kWarps; ++w) {
+                const int c = sGrp[w * E + e];
+                sGrp[w * E + e] = run;
+                run += c;
+            }
+            sRun[e] = run;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {   // (C)
+            if (j >= K) break;
+            const int e = mye[j];
+            int rank = 0;
+            for (int t2 = 0; t2 < kGateTok; ++t2) {
+#pragma unroll
+                for (int j2 = 0; j2 < 8; ++j2) {
+                    if (j2 >= K) break;
+                    const int e2 = __shfl_sync(0xffffffffu, mye[j2], t2);
+                    if (t2 < lane && e2 == e) ++rank;
+                }
+            }
+            if (valid) {
+                const int slot = sGrp[warp * E + e] + rank;
+                if (slot < C) {
+                    R.pick_slot[(size_t)tok * K + j] = slot;
+                    R.tbl_tok[(size_t)e * C + slot] = tok;
+                    R.tbl_w[(size_t)e * C + slot] = myw[j];
+                } else {
+                    R.pick_slot[(size_t)tok * K + j] = -1;
+                }
+            }
+        }
+        __syncthreads();   // sGrp is reused by the next group
+    }
+    // these blocks' picks/slots/weights are final (every warp's writes precede the bar.sync above):
+    // fence + per-block epoch flags, which the combine (any CTA of this rank) acquires
+    for (int blk = b0 + tid; blk < b1; blk += kThreads) {
+        __threadfence();
+        st_release_gpu_u32(R.blk_ready + blk, P.epoch);
     }
     __syncthreads();
+}
 
-    // push kept rows to the owner's receive buffer (one warp per (token, pick))
-    const int nunits = (tokB - tokA) * K;
+// Row push (runtime.hpp:341-372), after a second rank barrier (the slot table T_phi is complete):
+// the kept rows of this rank, flattened in (expert, slot) order, are split evenly across its CTAs.
+// Balanced — with slots taken in ascending token order, the low token ranges own almost every kept
+// row, so pushing by token range left half the CTAs idle — and progressive: CTA c covers a
+// contiguous run of experts, so the first experts' packets complete (and their FFN tiles start)
+// while later experts are still in flight. One warp per row, 16-byte peer stores, tf32 hi/lo split
+// (FP32) or bf16; the CTA completing a packet publishes its release signal (pgas.hpp:99-113).
+constexpr int kPushUnroll = 8;
+
+__device__ void push_phase(const LaunchParams& P, const RankCtx& R, const float* __restrict__ A, int cta,
+                           uint8_t* smem) {
+    const int E = P.E, H = P.H, C = P.C;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int* sN = reinterpret_cast<const int*>(smem) + kMaxExperts;   // n_e (dispatch_phase)
+    int* sOff = reinterpret_cast<int*>(smem) + 3 * kMaxExperts;        // [E + 1] prefix of n_e
+    int* sMine = sOff + kMaxExperts + 1;                                // rows of e pushed by this CTA
+    const uint32_t par = P.epoch & 1u;
+    const uint64_t sig_hi = (uint64_t)P.epoch << 32;
+    const uint64_t t_disp0 = globaltimer();
+    const bool straggle = P.straggler_rank == R.rank;
+    // straggler (runtime.hpp:358-362): packet e's signal is held back until its cumulative delay
+    auto hold = [&](int e) {
+        if (!straggle) return;
+        const uint64_t until = t_disp0 + R.delay_ns[e];
+        while (globaltimer() < until) {
+            if (ld_volatile_u32(P.abort_flag)) return;
+            __nanosleep(1000);
+        }
+    };
+    if (tid == 0) {
+        int acc = 0;
+        for (int e = 0; e < E; ++e) { sOff[e] = acc; acc += sN[e]; }
+        sOff[E] = acc;
+    }
+    __syncthreads();
+    const int total = sOff[E];
+    const int f0 = (int)((long long)total * cta / P.ctas_per_rank);
+    const int f1 = (int)((long long)total * (cta + 1) / P.ctas_per_rank);
+    for (int e = tid; e < E; e += kThreads) sMine[e] = max(0, min(f1, sOff[e + 1]) - max(f0, sOff[e]));
     const int H4 = H >> 2;
-    for (int u = warp; u < nunits; u += kThreads / 32) {
-        const int tok = tokA + u / K, j = u % K;
-        const int slot = R.pick_slot[(size_t)tok * K + j];
-        if (slot < 0) continue;
-        const int e = R.pick_e[(size_t)tok * K + j];
+    for (int f = f0 + warp; f < f1; f += kThreads / 32) {
+        int e = 0;   // expert of flattened row f: last e with sOff[e] <= f (binary search)
+        for (int lo = 0, hi = E; lo < hi;) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (mid < E && sOff[mid] <= f) { e = mid; lo = mid; } else hi = mid - 1;
+        }
+        const int slot = f - sOff[e];
+        const int tok = R.tbl_tok[(size_t)e * C + slot];
         const int q = e / P.El, le = e % P.El;
         const size_t row = (size_t)le * P.RP + (size_t)R.rank * P.Cp + slot;
         const float4* src = reinterpret_cast<const float4*>(A + (size_t)tok * H);
         uint8_t* hb = R.peer_heap[q];
-        if (P.prec == kFP32) {
-            float4* dhi = reinterpret_cast<float4*>(hb + R.hl.x[par][0]) + row * H4;
-            float4* dlo = reinterpret_cast<float4*>(hb + R.hl.x[par][1]) + row * H4;
-            for (int c = lane; c < H4; c += 32) {
-                const float4 v = __ldg(src + c);
-                float4 h, l;
-                h.x = tf32_hi(v.x); h.y = tf32_hi(v.y); h.z = tf32_hi(v.z); h.w = tf32_hi(v.w);
-                l.x = __fsub_rn(v.x, h.x); l.y = __fsub_rn(v.y, h.y);
-                l.z = __fsub_rn(v.z, h.z); l.w = __fsub_rn(v.w, h.w);
-                dhi[c] = h;
-                dlo[c] = l;
-            }
-        } else {
-            uint2* d = reinterpret_cast<uint2*>(hb + R.hl.x[par][0]) + row * H4;
-            for (int c = lane; c < H4; c += 32) {
-                const float4 v = __ldg(src + c);
-                __nv_bfloat162 p0 = __floats2bfloat162_rn(v.x, v.y);
-                __nv_bfloat162 p1 = __floats2bfloat162_rn(v.z, v.w);
-                uint2 o;
-                o.x = *reinterpret_cast<uint32_t*>(&p0);
-                o.y = *reinterpret_cast<uint32_t*>(&p1);
-                d[c] = o;
+        // kPushUnroll 16-byte loads per lane are issued before any store: one HBM latency per group
+        // instead of one per element (the loop would otherwise be latency-bound at ~1 us per load)
+        for (int c0 = lane; c0 < H4; c0 += 32 * kPushUnroll) {
+            float4 v[kPushUnroll];
+#pragma unroll
+            for (int u = 0; u < kPushUnroll; ++u)
+                if (c0 + 32 * u < H4) v[u] = __ldg(src + c0 + 32 * u);
+            if (P.prec == kFP32) {
+                float4* dhi = reinterpret_cast<float4*>(hb + R.hl.x[par][0]) + row * H4;
+                float4* dlo = reinterpret_cast<float4*>(hb + R.hl.x[par][1]) + row * H4;
+#pragma unroll
+                for (int u = 0; u < kPushUnroll; ++u) {
+                    if (c0 + 32 * u >= H4) break;
+                    float4 h, l;
+                    h.x = tf32_hi(v[u].x); h.y = tf32_hi(v[u].y); h.z = tf32_hi(v[u].z); h.w = tf32_hi(v[u].w);
+                    l.x = __fsub_rn(v[u].x, h.x); l.y = __fsub_rn(v[u].y, h.y);
+                    l.z = __fsub_rn(v[u].z, h.z); l.w = __fsub_rn(v[u].w, h.w);
+                    dhi[c0 + 32 * u] = h;
+                    dlo[c0 + 32 * u] = l;
+                }
+            } else {
+                uint2* d = reinterpret_cast<uint2*>(hb + R.hl.x[par][0]) + row * H4;
+#pragma unroll
+                for (int u = 0; u < kPushUnroll; ++u) {
+                    if (c0 + 32 * u >= H4) break;
+                    __nv_bfloat162 p0 = __floats2bfloat162_rn(v[u].x, v[u].y);
+                    __nv_bfloat162 p1 = __floats2bfloat162_rn(v[u].z, v[u].w);
+                    uint2 o;
+                    o.x = *reinterpret_cast<uint32_t*>(&p0);
+                    o.y = *reinterpret_cast<uint32_t*>(&p1);
+                    d[c0 + 32 * u] = o;
+                }
             }
         }
     }
     __syncthreads();
-    // one system-scope fence orders every row this CTA pushed (cumulative through bar.sync)
-    // before the packet counters below; the last CTA to complete a packet publishes its signal
-    // with release semantics (pgas.hpp:99-113)
+    // one system-scope fence orders every row this CTA pushed (cumulative through bar.sync) before
+    // the packet counters below; the last CTA to complete a packet publishes its signal
     if (tid == 0) __threadfence_system();
     __syncthreads();
     for (int e = tid; e < E; e += kThreads) {
-        const int kept = sKept[e];
+        const int kept = sMine[e];
         if (kept <= 0) continue;
         const uint32_t old = atomicAdd(&R.sent[e], (uint32_t)kept);
         if ((int)(old + kept) == sN[e]) {
@@ -1697,12 +1773,17 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
     if (!rank_barrier(P, R, P.launch_seq)) goto done;
     if (tid == 0) trace[2] = globaltimer();
 
-    // phase 2: slot assignment + dispatch
+    // phase 2: slot assignment, then (after the slot table is complete) the balanced row push
     dispatch_phase(P, R, A, cta, smem);
+    if (tid == 0) trace[kTrSlots] = globaltimer();
+    if (!rank_barrier(P, R, P.launch_seq + 1)) goto done;
+    if (tid == 0) trace[kTrSlotBarrier] = globaltimer();
+    push_phase(P, R, A, cta, smem);
     __syncthreads();
+    if (tid == 0) trace[kTrPush] = globaltimer();
     for (int e = tid; e < P.E; e += kThreads) s_n_expert[e] = reinterpret_cast<const int*>(smem)[kMaxExperts + e];
     // sequential schedule: every rank's dispatch lands before any expert tile starts
-    if (P.sequential && !group_barrier(P, R, P.launch_seq + 1, 0, cta)) goto done;
+    if (P.sequential && !group_barrier(P, R, P.launch_seq + 2, 0, cta)) goto done;
     if (tid == 0) trace[3] = globaltimer();
 
     // phase 3: expert FFN tiles
@@ -1730,7 +1811,7 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
     }
     __syncthreads();
     // sequential schedule: every rank's expert compute drains before any combine starts
-    if (P.sequential && !group_barrier(P, R, P.launch_seq + 3, 1, cta)) goto done;
+    if (P.sequential && !group_barrier(P, R, P.launch_seq + 4, 1, cta)) goto done;
     if (tid == 0) trace[4] = globaltimer();
 
     // phase 4: combine

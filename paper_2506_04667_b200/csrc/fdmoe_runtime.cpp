@@ -589,7 +589,7 @@ static fdmoe_status launch_all(fdmoe_handle* h, const float* const* in_dev, floa
         CK(cudaEventRecord(g.ev0, s));
         CK(launch_layer(p, g.ctas_per_rank * (int)g.members.size(), g.smem, s));
         CK(cudaEventRecord(g.ev1, s));
-        g.launch_seq += sequential ? 1 + 2 * kGroupBarriers : 1;   // rank-barrier generations used
+        g.launch_seq += sequential ? 2 + 2 * kGroupBarriers : 2;   // rank-barrier generations used
     }
     h->in_flight = true;
     return FDMOE_OK;

@@ -17,6 +17,8 @@ names = ["start", "gate", "barrier", "dispatch", "ffn", "combine", "end"]
 print("kernel ms", op.last_kernel_ms())
 for i, n in enumerate(names):
     print(f"{n:9s} min {t[:, i].min():9.1f}  med {np.median(t[:, i]):9.1f}  max {t[:, i].max():9.1f} us")
+for i, n in ((20, "prefix"), (21, "slots"), (22, "slot-barrier"), (23, "push")):
+    print(f"{n:12s} min {t[:, i].min():9.1f}  med {np.median(t[:, i]):9.1f}  max {t[:, i].max():9.1f} us")
 print("ffn tiles per CTA: min", int(t[:, 7].min()), "max", int(t[:, 7].max()), "sum", int(t[:, 7].sum()))
 ffn_cyc = (t[:, 4] - t[:, 3]).mean() * 1e3 * 1.965   # ns -> cycles at max clock (approx)
 for i, n in enumerate(["mma<-tokens", "mma<-weights", "mma<-acc", "conv<-wTMA", "conv<-tmemA", "prod<-wslot", "prod<-xslot", "epi<-acc"]):
