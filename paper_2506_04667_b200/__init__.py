@@ -112,7 +112,8 @@ class _Stats(C.Structure):
 class _Info(C.Structure):
     _fields_ = [("capacity", C.c_int64), ("packet_rows", C.c_int64), ("heap_bytes", C.c_int64),
                 ("scratch_bytes", C.c_int64), ("weight_bytes", C.c_int64), ("ctas_per_rank", C.c_int32),
-                ("smem_bytes", C.c_int32), ("num_sms", C.c_int32), ("ranks_per_launch", C.c_int32)]
+                ("smem_bytes", C.c_int32), ("num_sms", C.c_int32), ("ranks_per_launch", C.c_int32),
+                ("fused_combine", C.c_int32)]
 
 
 EXPORTED_SYMBOLS = [

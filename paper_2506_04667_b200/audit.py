@@ -10,7 +10,8 @@ a combine task is a block of 16 tokens — trace.py documents the event fields):
   (c) dependency order  every (source, expert) packet's signal precedes the GEMM0 tiles reading it;
                         all GEMM0 tiles of a row tile end before any of its GEMM1 tiles starts; every
                         GEMM1 tile put into an origin precedes that origin's combine tasks
-                        (audit.hpp:102-160)
+                        (audit.hpp:102-160; with the combine fused into the GEMM1 epilogues there are
+                        neither puts nor combine tasks)
   (d) single launch     one launch per rank, every CTA spawned exactly once (audit.hpp:170-186)
   (e) phase gating      sequential mode only: no expert tile starts before every rank's last
                         dispatch signal, no combine starts before every rank's last GEMM1 tile
@@ -77,14 +78,16 @@ def tile_rows(cfg, gates, rank: int) -> Dict[Tuple[int, int], Tuple[int, int, in
     return out
 
 
-def expected_task_keys(cfg, gates, rank: int) -> List[str]:
-    """Canonical keys of every task `rank` must execute (the closed-form recount)."""
+def expected_task_keys(cfg, gates, rank: int, fused_combine: bool = False) -> List[str]:
+    """Canonical keys of every task `rank` must execute (the closed-form recount). With the combine
+    fused into the GEMM1 epilogues there are no separate combine tasks."""
     nb0, nb1 = -(-cfg.ffn_dim // BF), -(-cfg.embed_dim // BF)
     keys = []
     for (le, m), (s0, _, _) in tile_rows(cfg, gates, rank).items():
         keys += [f"gemm0:s{s0}:e{le}:r{m}:c{c}" for c in range(nb0)]
         keys += [f"gemm1:s{s0}:e{le}:r{m}:c{c}" for c in range(nb1)]
-    keys += [f"combine:s{rank}:e-1:r{t}:c-1" for t in range(-(-cfg.tokens_per_device // COMBINE_TOK))]
+    if not fused_combine:
+        keys += [f"combine:s{rank}:e-1:r{t}:c-1" for t in range(-(-cfg.tokens_per_device // COMBINE_TOK))]
     return sorted(keys)
 
 
@@ -92,22 +95,22 @@ def _key(e: TraceEvent) -> str:
     return f"{e.task_type}:s{e.src}:e{e.expert}:r{e.rb}:c{e.cb}"
 
 
-def check_exactly_once(res, cfg, rep: Report, ranks: Sequence[int]):
+def check_exactly_once(res, cfg, rep: Report, ranks: Sequence[int], fused_combine: bool = False):
     for d in ranks:
         executed = sorted(_key(e) for e in res.trace if e.device == d and e.event == "exec")
-        expected = expected_task_keys(cfg, res.gates, d)
+        expected = expected_task_keys(cfg, res.gates, d, fused_combine)
         if executed != expected:
             dup = [k for k, n in collections.Counter(executed).items() if n > 1]
             rep.fail(f"device {d}: executed {len(executed)} tasks, expected {len(expected)}"
                      f" ({len(set(expected) - set(executed))} missing, {len(dup)} duplicated)")
 
 
-def check_accounting(res, cfg, rep: Report, ranks: Sequence[int]):
+def check_accounting(res, cfg, rep: Report, ranks: Sequence[int], fused_combine: bool = False):
     nb0, nb1 = -(-cfg.ffn_dim // BF), -(-cfg.embed_dim // BF)
     for i, d in enumerate(ranks):
         st = res.stats[i]
         tiles = len(tile_rows(cfg, res.gates, d))
-        want = (tiles * nb0, tiles * nb1, -(-cfg.tokens_per_device // COMBINE_TOK))
+        want = (tiles * nb0, tiles * nb1, 0 if fused_combine else -(-cfg.tokens_per_device // COMBINE_TOK))
         got = (st.gemm0, st.gemm1, st.combine)
         if got != want:
             rep.fail(f"device {d}: stats gemm0/gemm1/combine={got}, recount={want}")
@@ -192,16 +195,19 @@ def check_phase_gating(res, rep: Report, sequential: bool):
 
 
 def full_audit(res, cfg, sequential: bool = False, ranks: Optional[Sequence[int]] = None,
-               ctas_per_rank: Optional[int] = None, same_clock: bool = True) -> Report:
-    """audit.hpp full_audit over a ForwardResult whose trace was recorded (ForwardOptions(trace=True))."""
+               ctas_per_rank: Optional[int] = None, same_clock: bool = True, fused_combine: bool = False) -> Report:
+    """audit.hpp full_audit over a ForwardResult whose trace was recorded (ForwardOptions(trace=True)).
+    fused_combine: the launch folded the combine into the GEMM1 epilogues (Operator.info()
+    ["fused_combine"] and an overlapped schedule): no combine tasks, no tile puts."""
+    fused_combine = fused_combine and not sequential
     ranks = list(range(cfg.devices)) if ranks is None else list(ranks)
     rep = Report()
     if not res.trace:
         rep.fail("empty trace: run the forward with ForwardOptions(trace=True)")
         return rep
-    check_exactly_once(res, cfg, rep, ranks)
+    check_exactly_once(res, cfg, rep, ranks, fused_combine)
     if res.stats:
-        check_accounting(res, cfg, rep, ranks)
+        check_accounting(res, cfg, rep, ranks, fused_combine)
     check_dependencies(res, cfg, rep, ranks, same_clock)
     check_single_launch(res, rep, ranks, ctas_per_rank)
     check_phase_gating(res, rep, sequential)

@@ -99,6 +99,7 @@ struct alignas(64) RankCtx {
     const unsigned long long* delay_ns;   // [E_total] straggler: cumulative hold-back of packet e's signal
     DevEvent* ev;              // [ev_cap] device event log (fdmoe_event layout)
     uint32_t* ev_ctr;          // records emitted this launch (reset by the host before the launch)
+    uint32_t* zero_ctr;        // fused combine: CTAs whose output rows are zeroed (monotonic)
     uint32_t ev_cap;
     int32_t rank;
 };
@@ -118,6 +119,10 @@ struct LaunchParams {
     int sequential;            // bulk-synchronous schedule (group barrier after dispatch and after the FFN)
     int trace_events;          // record the device event log
     int straggler_rank;        // rank whose packet signals are held back by delay_ns (-1: none)
+    uint32_t zero_target;      // fused combine: zero_ctr value once every CTA of this launch zeroed its rows
+    int fused_combine;         // 1: GEMM1 epilogues accumulate w * y straight into the origin's output
+                               //    (k <= 2: fl(fl(w0 y0) + fl(w1 y1)) is order-free; all ranks of the
+                               //    group on this device; overlapped schedule) -- no combine phase
     int debug;                 // ablation bits (FDMOE_DEBUG env; 0 in production): see kDbg*
     int exact_gate;            // 1: reference-exact logits for every token (bit-exact G_phi, weights)
     float gate_u;              // certified gate: u' = 2^-24 * 1.001

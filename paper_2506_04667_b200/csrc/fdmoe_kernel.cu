@@ -1501,7 +1501,7 @@ __device__ void gemm_mma(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, unsi
 }
 
 // warps 8-11: thread = output feature (TMEM lane), 32 token columns per tcgen05.ld
-template <int PREC>
+template <int PREC, bool FUSED>
 __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl& G, unsigned long long* stat,
                               unsigned long long* trace) {
     long long w_acc = 0, busy = 0;
@@ -1514,6 +1514,23 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
     uint32_t accphase = 0;
     const uint32_t tmem = G.tmem_base;
     const int e_glob_base = R.rank * P.El;
+    bool zero_seen = false;
+    if (FUSED) {
+        // fused combine accumulates into the output: zero this CTA's token rows while the first tile's
+        // MMAs run (streaming stores), then count this CTA in; GEMM1 epilogues wait for every CTA of
+        // the origin rank (the first GEMM1 tile starts long after, so the wait is free in practice)
+        const int cta = blockIdx.x % P.ctas_per_rank;
+        int tokA, tokB, b0, b1;
+        gate_token_range(P, cta, tokA, tokB, b0, b1);
+        float4* o4 = reinterpret_cast<float4*>(P.out[blockIdx.x / P.ctas_per_rank] + (size_t)tokA * P.H);
+        const size_t n4 = (size_t)(tokB - tokA) * P.H / 4;
+        for (size_t i = et; i < n4; i += 128) __stcs(o4 + i, make_float4(0.0f, 0.0f, 0.0f, 0.0f));
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (et == 0) {
+            __threadfence();
+            atomicAdd(R.zero_ctr, 1u);
+        }
+    }
     while (true) {
         if (!mbar_wait(&G.qfull[q], qphase, P.abort_flag)) return;
         const Task& tk = G.ring[q];   // stays valid until this warp group releases the slot
@@ -1524,6 +1541,11 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
         }
         if (!FD_TIMED_WAIT(w_acc, mbar_wait(&G.tfull[acc], accphase, P.abort_flag))) return;
         tc_fence_after();
+        if (FUSED && type == 1 && !zero_seen) {
+            for (int r = 0; r < P.nranks; ++r)
+                if (!wait_counter(P, R, P.ranks[r].zero_ctr, P.zero_target, 310)) return;
+            zero_seen = true;
+        }
         const long long tb0 = clk();
 
         const int ncols = type == 0 ? P.D : P.H;
@@ -1577,9 +1599,18 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
                     int src, slot;
                     if (P.Cp >= kBM) { src = src0; slot = rb_base + n; }
                     else { const int j = n / P.Cp; src = src0 + j; slot = n - j * P.Cp; }
-                    float* ydst = reinterpret_cast<float*>(R.peer_heap[src] + R.hl.yc) +
-                                  ((size_t)e_glob * P.C + slot) * P.H + feat;
-                    *ydst = v;
+                    if (FUSED) {
+                        // combine fused here (oracle.hpp:102-107 with k <= 2): O[t] += fl(w * y); the
+                        // origin's slot table gives the token and its combine weight
+                        const RankCtx& Ro = P.ranks[src];
+                        const size_t ts = (size_t)e_glob * P.C + slot;
+                        const int t = Ro.tbl_tok[ts];
+                        atomicAdd(P.out[src] + (size_t)t * P.H + feat, __fmul_rn(Ro.tbl_w[ts], v));
+                    } else {
+                        float* ydst = reinterpret_cast<float*>(R.peer_heap[src] + R.hl.yc) +
+                                      ((size_t)e_glob * P.C + slot) * P.H + feat;
+                        *ydst = v;
+                    }
                 }
             }
         }
@@ -1602,7 +1633,7 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
                 emit_event(P, R, kEvExec, cta, kTaskGemm1, tk.t0, globaltimer(), tk.src0, tk.le, tk.m, tk.nb,
                            tk.nsrc, rows);
                 const int rbf = P.Cp >= kBM ? (tk.m % (P.Cp / kBM)) : 0;
-                for (int j = 0; j < tk.nsrc; ++j) {
+                for (int j = 0; j < tk.nsrc && !FUSED; ++j) {
                     if (tk.cnt[j] <= 0) continue;
                     unsigned long long* f = reinterpret_cast<unsigned long long*>(R.peer_heap[tk.src0 + j] +
                                                                                   R.hl.cflag[par]) +
@@ -1807,15 +1838,20 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
         gemm_wconvert<PREC>(P, ring, G, trace,
                             (cta == 0 && warp == kWarpConv0 && R.chunklog) ? R.chunklog : nullptr);
     } else if (warp < 4) {
-        gemm_epilogue<PREC>(P, R, G, s_stat, trace);
+        if constexpr (PREC == kFP32) {
+            if (P.fused_combine) gemm_epilogue<PREC, true>(P, R, G, s_stat, trace);
+            else gemm_epilogue<PREC, false>(P, R, G, s_stat, trace);
+        } else {
+            gemm_epilogue<PREC, false>(P, R, G, s_stat, trace);
+        }
     }
     __syncthreads();
     // sequential schedule: every rank's expert compute drains before any combine starts
     if (P.sequential && !group_barrier(P, R, P.launch_seq + 4, 1, cta)) goto done;
     if (tid == 0) trace[4] = globaltimer();
 
-    // phase 4: combine
-    if (ld_volatile_u32(P.abort_flag) == 0) combine_phase(P, R, O, smem, s_n_expert, s_stat);
+    // phase 4: combine (fused into the GEMM1 epilogues when P.fused_combine)
+    if (!P.fused_combine && ld_volatile_u32(P.abort_flag) == 0) combine_phase(P, R, O, smem, s_n_expert, s_stat);
     if (tid == 0) trace[5] = globaltimer();
 
 done:

@@ -143,6 +143,7 @@ struct Group {
     int smem = 0;
     int num_sms = 0;
     unsigned long long launch_seq = 0;
+    uint32_t zero_seq = 0;          // fused-combine launches since the control block was cleared
 };
 
 // control block offsets
@@ -278,6 +279,7 @@ fdmoe_status build_ctx(fdmoe_handle* h) {
             c.ev = r.ev;
             c.ev_cap = r.ev_cap;
             c.ev_ctr = reinterpret_cast<uint32_t*>(r.ctrl + ctrl_ev_ctr(d));
+            c.zero_ctr = reinterpret_cast<uint32_t*>(r.ctrl + ctrl_ev_ctr(d) + 4);
             c.bar = reinterpret_cast<unsigned long long*>(r.ctrl + kCtrlBar);
             c.gemm_head = reinterpret_cast<uint32_t*>(r.ctrl + kCtrlGemm);
             c.comb_head = reinterpret_cast<uint32_t*>(r.ctrl + kCtrlComb);
@@ -326,6 +328,7 @@ fdmoe_status check_errors(fdmoe_handle* h) {
                 cudaMemset(h->ranks[idx].ctrl, 0, ctrl_bytes(h->dm));
             }
             g.launch_seq = 0;
+            g.zero_seq = 0;
         }
         return fail(worst, msg);
     }
@@ -569,6 +572,9 @@ static fdmoe_status launch_all(fdmoe_handle* h, const float* const* in_dev, floa
         p.sequential = sequential ? 1 : 0;
         p.trace_events = trace_events ? 1 : 0;
         p.straggler_rank = straggler_rank;
+        p.fused_combine = (d.prec == FDMOE_FP32 && d.k <= 2 && !sequential && (int64_t)g.members.size() == d.P &&
+                           h->n_local == d.P) ? 1 : 0;
+        if (p.fused_combine) p.zero_target = (++g.zero_seq) * (uint32_t)g.ctas_per_rank;
         p.exact_gate = (opts && opts->exact_gate) ? 1 : 0;
         {   // certified-gate bound coefficients (fdmoe_kernel.cu, phase 1)
             const double u = std::ldexp(1.0, -24), n1 = (double)d.H + 1.0;
@@ -788,6 +794,8 @@ fdmoe_status fdmoe_get_info(fdmoe_handle* h, fdmoe_info* info) {
     info->smem_bytes = h->groups[0].smem;
     info->num_sms = h->groups[0].num_sms;
     info->ranks_per_launch = (int32_t)h->groups[0].members.size();
+    info->fused_combine = (h->dm.prec == FDMOE_FP32 && h->dm.k <= 2 &&
+                           (int64_t)h->groups[0].members.size() == h->dm.P && h->n_local == h->dm.P) ? 1 : 0;
     return FDMOE_OK;
 }
 

@@ -51,7 +51,8 @@ def test_sequential_mode_matches_overlapped(P, E, S):
 def test_event_log_passes_audits(P, E, S, prec, sequential, tmp_path):
     cfg = _cfg(P, E, S, prec=prec)
     res, info, _, _, _ = _run(cfg, fd.ForwardOptions(sequential=sequential, trace=True))
-    rep = audit.full_audit(res, cfg, sequential=sequential, ctas_per_rank=info["ctas_per_rank"])
+    rep = audit.full_audit(res, cfg, sequential=sequential, ctas_per_rank=info["ctas_per_rank"],
+                           fused_combine=bool(info["fused_combine"]))
     assert rep.ok(), rep.problems[:5]
     assert (audit.barrier_event_count(res) > 0) == sequential
     bf = busy_fractions(res.trace)
@@ -100,7 +101,7 @@ def test_straggler_holds_back_dispatch():
     assert len(sig) == cfg.experts_total
     for e, t in sig.items():
         assert t - gate_end >= int(hold[e]) * 0.95, (e, t - gate_end, int(hold[e]))
-    assert audit.full_audit(res, cfg).ok()
+    assert audit.full_audit(res, cfg, fused_combine=True).ok()
 
 
 def test_lognormal_straggler_sequential_slower_than_overlapped():
