@@ -731,6 +731,68 @@ __device__ void gate_pairs_exact(const LaunchParams& P, const RankCtx& R, const 
     __syncthreads();
 }
 
+// Full exact pass (ties / near-ties): every expert's reference logit of the nf tokens in sFull -> sL
+// rows [0, nf). Thread e runs expert e's chain z = sum over x ascending of fl(a_x * w_xe)
+// (gate.hpp:77-81) over Wg rows that stream through shared memory in X-row chunks (cp.async,
+// double-buffered, coalesced; the token's x-chunk rides along). The chain loop is unrolled so its
+// shared loads are off the FADD dependency: ~4 cycles per x, one H-long chain per expert.
+__device__ void gate_full_exact(const LaunchParams& P, const RankCtx& R, const float* __restrict__ A,
+                                const GateSmem& g, int nf) {
+    const int E = P.E, H = P.H, Ep = (E + 7) & ~7, tid = threadIdx.x;
+    const int cap = kGateRegionFloats - g.sub * Ep;   // floats after sL (the cp.async staging area)
+    int X = (cap / (2 * (Ep + 1))) & ~31;
+    X = X < 32 ? 32 : (X > 256 ? 256 : X);
+    float* buf = g.sA;   // [2][X][Ep] Wg rows, then [2][X] token values
+    float* abuf = buf + 2 * X * Ep;
+    const bool vec = (E & 3) == 0;
+    const int nch = (H + X - 1) / X;   // H % 32 == 0 (envelope), X % 32 == 0: whole 16-byte groups
+    for (int t = 0; t < nf; ++t) {
+        const float* a = A + (size_t)g.sFull[t] * H;
+        auto load = [&](int st, int c) {
+            const int x0 = c * X, xn = min(X, H - x0);
+            float* b = buf + st * X * Ep;
+            if (vec) {
+                const int cpr = E >> 2;
+                for (int i = tid; i < xn * cpr; i += kThreads) {
+                    const int xx = i / cpr, q = i - xx * cpr;
+                    cp_async16(b + xx * Ep + 4 * q, R.wg + (size_t)(x0 + xx) * E + 4 * q, true);
+                }
+            } else {
+                for (int i = tid; i < xn * E; i += kThreads) {
+                    const int xx = i / E, e = i - xx * E;
+                    b[xx * Ep + e] = R.wg[(size_t)(x0 + xx) * E + e];
+                }
+            }
+            for (int i = tid; i < xn / 4; i += kThreads) cp_async16(abuf + st * X + 4 * i, a + x0 + 4 * i, true);
+            cp_async_commit();
+        };
+        float acc = 0.0f;
+        __syncthreads();   // sL / staging area free (callers' previous use is done)
+        load(0, 0);
+        for (int c = 0; c < nch; ++c) {
+            if (c + 1 < nch) load((c + 1) & 1, c + 1); else cp_async_commit();
+            cp_async_wait<1>();
+            __syncthreads();
+            const int xn = min(X, H - c * X);
+            const float* b = buf + (c & 1) * X * Ep + tid;
+            const float* av = abuf + (c & 1) * X;
+            if (tid < E) {
+                for (int xx = 0; xx < xn; xx += 8) {   // xn % 32 == 0
+                    float w[8], x[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) { w[u] = b[(xx + u) * Ep]; x[u] = av[xx + u]; }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) acc = __fadd_rn(acc, __fmul_rn(x[u], w[u]));
+                }
+            }
+            __syncthreads();   // buffer (c & 1) is refilled by the next iteration's load
+        }
+        cp_async_wait<0>();
+        if (tid < E) g.sL[t * Ep + tid] = acc;
+    }
+    __syncthreads();
+}
+
 // Decide a token from its candidates' exact logits (one warp). false: ties / near-ties -> full exact.
 __device__ bool route_resolve(const LaunchParams& P, const RankCtx& R, float* row, int tok, int t, const GateSmem& g) {
     const int K = P.k, lane = threadIdx.x & 31;
@@ -831,7 +893,7 @@ __device__ void gate_phase(const LaunchParams& P, const RankCtx& R, const float*
         }
         const int nf = s_nfull;
         if (nf > 0 && !(P.debug & kDbgGateNoFlush)) {   // ties / near-ties / overflow: the reference chain for all E
-            gate_logits<false, 1, 4>(P, R, A, 0, g.sFull, nf, g);
+            gate_full_exact(P, R, A, g, nf);
             for (int t = warp; t < nf; t += kWarps) route_exact(P, R, g.sL + t * Ep, g.sFull[t], g.sCnt);
             n_full += nf;
         }
