@@ -714,6 +714,7 @@ __device__ void gate_pairs_exact(const LaunchParams& P, const RankCtx& R, const 
             if (tid < nb) {
                 const float* b = g.sPair + (ch & 1) * kGatePairBatch * kGatePairPitch + tid * kGatePairPitch;
                 const int xl = min(kGatePairX, H - ch * kGatePairX);
+#pragma unroll 4   // loads of the next groups issue ahead of this group's dependent FADDs
                 for (int x = 0; x < xl; x += 4) {
                     const float4 a4 = *reinterpret_cast<const float4*>(b + x);
                     const float4 w4 = *reinterpret_cast<const float4*>(b + kGatePairX + x);
