@@ -1172,15 +1172,15 @@ template <int PREC>
 struct GemmCfg {
     static constexpr int ESZ = PREC == kFP32 ? 4 : 2;
     static constexpr int ATOM_K = 128 / ESZ;                    // K elements per 128-byte atom row
-    static constexpr int NATOM = 1;
+    static constexpr int NATOM = 2;
     static constexpr int BK = ATOM_K * NATOM;                   // K per stage (64 fp32 / 128 bf16)
     static constexpr int ATOM_BYTES = 128 * 128;                // 128 rows x 128 B
     static constexpr int PLANE_BYTES = ATOM_BYTES * NATOM;      // one operand plane per stage (32 KB)
     static constexpr int PLANES = PREC == kFP32 ? 2 : 1;        // hi/lo split of the token operand
     static constexpr int STAGE_BYTES = PLANE_BYTES * PLANES;   // token stage
-    static constexpr int STAGES = PREC == kFP32 ? 4 : 6;       // token smem ring == weight TMEM ring
+    static constexpr int STAGES = PREC == kFP32 ? 2 : 3;       // token smem ring == weight TMEM ring
     static constexpr int W_BYTES = PLANE_BYTES;                 // weight stage (raw FP32 / bf16)
-    static constexpr int WSTAGES = PREC == kFP32 ? 4 : 6;      // weight smem ring (TMA -> converters)
+    static constexpr int WSTAGES = PREC == kFP32 ? 2 : 3;      // weight smem ring (TMA -> converters)
     static constexpr int KSTEP = PREC == kFP32 ? 8 : 16;       // K per tcgen05.mma
     static constexpr int KSTEPS = BK / KSTEP;                   // 8
     static constexpr int STEPS_PER_ATOM = ATOM_K / KSTEP;       // 4
@@ -1527,7 +1527,7 @@ __device__ void gemm_mma(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, unsi
         long long t_rdy = chunklog ? clk() : 0;
         if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.ready[stage], phase, P.abort_flag))) return;
         tc_fence_after();
-#pragma unroll 4   // fewer loop back-edges (and their YIELDs) between stages: measured best of 1/4/8/16
+#pragma unroll 4   // fewer loop back-edges (and their YIELDs) between stages (measured: 4 beats 1/2/8/16)
         for (int kb = 0; kb < nk; ++kb) {
             const long long t_iss = chunklog ? clk() : 0;
             const uint32_t abase = tmem + Cfg::TMEM_A0 + stage * Cfg::A_COLS;
