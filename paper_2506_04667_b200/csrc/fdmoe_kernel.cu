@@ -866,8 +866,13 @@ __device__ void gate_phase(const LaunchParams& P, const RankCtx& R, const float*
         const int s0 = (int)((long long)ntok * si / nsub);
         const int s1 = (int)((long long)ntok * (si + 1) / nsub);
         const int ts = s1 - s0;
+        // few tokens per CTA (small S or many CTAs per rank): the 5 x 8 thread tile would leave most
+        // threads idle (c5: 6 of 384 active), so switch to 1 token x 4 experts per thread
+        const bool small = ((ts + kGateTT - 1) / kGateTT) * (Ep / kGateTE) * 4 <= kThreads &&
+                           ts * (Ep / 4) <= kThreads;   // ... and the small tile covers the sub-tile in one round
         if (P.exact_gate) {
-            gate_logits<false, kGateTT, kGateTE>(P, R, A, tokA + s0, nullptr, ts, g);
+            if (small) gate_logits<false, 1, 4>(P, R, A, tokA + s0, nullptr, ts, g);
+            else gate_logits<false, kGateTT, kGateTE>(P, R, A, tokA + s0, nullptr, ts, g);
             for (int t = warp; t < ts; t += kWarps) route_exact(P, R, g.sL + t * Ep, tokA + s0 + t, g.sCnt);
             n_full += ts;
             continue;
@@ -875,7 +880,8 @@ __device__ void gate_phase(const LaunchParams& P, const RankCtx& R, const float*
         for (int t = tid; t < ts; t += kThreads) { g.sSab[t] = 0.0f; g.sTNC[t] = 0; }
         if (tid == 0) { s_np = 0; s_nfull = 0; }
         __syncthreads();
-        gate_logits<true, kGateTT, kGateTE>(P, R, A, tokA + s0, nullptr, ts, g);
+        if (small) gate_logits<true, 1, 4>(P, R, A, tokA + s0, nullptr, ts, g);
+        else gate_logits<true, kGateTT, kGateTE>(P, R, A, tokA + s0, nullptr, ts, g);
         for (int t = warp; t < ts; t += kWarps) {
             const int r = route_certified(P, R, g.sL + t * Ep, tokA + s0 + t, t, g, &s_np);
             if (r == 2 && (tid & 31) == 0) g.sFull[atomicAdd(&s_nfull, 1)] = tokA + s0 + t;
