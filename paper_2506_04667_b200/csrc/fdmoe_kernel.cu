@@ -1572,7 +1572,8 @@ __device__ void gemm_mma(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, unsi
 // warps 8-11: thread = output feature (TMEM lane), 32 token columns per tcgen05.ld
 template <int PREC, bool FUSED>
 __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl& G, unsigned long long* stat,
-                              unsigned long long* trace) {
+                              unsigned long long* trace, unsigned long long* elog) {
+    int nelog = 0;
     long long w_acc = 0, busy = 0;
     const int et = threadIdx.x;   // warps 0-3: 0..127 == TMEM lane == feature row in the tile
     const int wq = et >> 5;
@@ -1616,6 +1617,7 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
             zero_seen = true;
         }
         const long long tb0 = clk();
+        long long e_loop = 0, e_bar = 0, e_ld = 0;
 
         const int ncols = type == 0 ? P.D : P.H;
         const int feat = tk.nb * kBF + et;
@@ -1630,9 +1632,35 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
         float* c1hi = reinterpret_cast<float*>(R.c1[0]) + grow0 * (size_t)P.D + feat;
         float* c1lo = reinterpret_cast<float*>(R.c1[1]) + grow0 * (size_t)P.D + feat;
         __nv_bfloat16* c1b = reinterpret_cast<__nv_bfloat16*>(R.c1[0]) + grow0 * (size_t)P.D + feat;
+        // GEMM1 row metadata, one row per lane per 32-row chunk, all loads issued together at tile start
+        // (a per-row chain of dependent loads inside the element loop cost ~600 cycles per row):
+        // fused: the origin's output row pointer and combine weight; else the origin's yc row pointer
+        const int lane = et & 31;
+        float* rowp[kNT / 32];
+        float roww[kNT / 32];
+        if (type == 1) {
+#pragma unroll
+            for (int c = 0; c < kNT / 32; ++c) {
+                const int n = c * 32 + lane;
+                int src, slot;
+                if (P.Cp >= kBM) { src = src0; slot = rb_base + n; }
+                else { const int j = n / P.Cp; src = min(src0 + j, P.P - 1); slot = n - j * P.Cp; }
+                const size_t ts = (size_t)e_glob * P.C + min(slot, P.C - 1);
+                if (FUSED) {
+                    const RankCtx& Ro = P.ranks[src];
+                    const int t = Ro.tbl_tok[ts];
+                    roww[c] = Ro.tbl_w[ts];
+                    rowp[c] = P.out[src] + (size_t)max(t, 0) * P.H;
+                } else {
+                    roww[c] = 0.0f;
+                    rowp[c] = reinterpret_cast<float*>(R.peer_heap[src] + R.hl.yc) + ts * P.H;
+                }
+            }
+        }
 #pragma unroll 1
         for (int ch = 0; ch < kNT / 32; ++ch) {
             uint32_t r[32];
+            const long long tl0 = clk();
             tmem_ld32(tbase + ch * 32, r);
             // validity of the 32 token rows of this chunk: bit i = row ch*32+i holds a landed token
             uint32_t vmask;
@@ -1648,6 +1676,7 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
                 }
             }
             tmem_wait_ld();
+            e_ld += clk() - tl0;
             if (!fvalid || (P.debug & kDbgNoEpiStore)) vmask = 0;
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
@@ -1665,26 +1694,24 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
                         c1b[o] = __float2bfloat16_rn(v);
                     }
                 } else {
-                    int src, slot;
-                    if (P.Cp >= kBM) { src = src0; slot = rb_base + n; }
-                    else { const int j = n / P.Cp; src = src0 + j; slot = n - j * P.Cp; }
+                    // row n's pointer (and weight) from lane i of this chunk's prefetch
+                    float* rp = reinterpret_cast<float*>(
+                        __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(rowp[ch]), i));
                     if (FUSED) {
                         // combine fused here (oracle.hpp:102-107 with k <= 2): O[t] += fl(w * y); the
                         // origin's slot table gives the token and its combine weight
-                        const RankCtx& Ro = P.ranks[src];
-                        const size_t ts = (size_t)e_glob * P.C + slot;
-                        const int t = Ro.tbl_tok[ts];
-                        atomicAdd(P.out[src] + (size_t)t * P.H + feat, __fmul_rn(Ro.tbl_w[ts], v));
+                        const float w = __shfl_sync(0xffffffffu, roww[ch], i);
+                        atomicAdd(rp + feat, __fmul_rn(w, v));
                     } else {
-                        float* ydst = reinterpret_cast<float*>(R.peer_heap[src] + R.hl.yc) +
-                                      ((size_t)e_glob * P.C + slot) * P.H + feat;
-                        *ydst = v;
+                        rp[feat] = v;
                     }
                 }
             }
         }
+        e_loop = clk();
         tc_fence_before();
         asm volatile("bar.sync 1, 128;" ::: "memory");   // all rows stored, TMEM drained
+        e_bar = clk();
         if (et == 0) {
             mbar_arrive(&G.tempty[acc]);
             int rows = 0;
@@ -1697,7 +1724,8 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
                 atomicAdd(R.g0done + (size_t)tk.le * P.MT + tk.m, 1u);
                 stat[0]++;
             } else {
-                __threadfence_system();
+                // the tile's rows went to the origin rank: system scope when it may be another GPU
+                if (P.nranks == P.P) __threadfence(); else __threadfence_system();
                 const int cta = blockIdx.x % P.ctas_per_rank;
                 emit_event(P, R, kEvExec, cta, kTaskGemm1, tk.t0, globaltimer(), tk.src0, tk.le, tk.m, tk.nb,
                            tk.nsrc, rows);
@@ -1716,6 +1744,10 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
             mbar_arrive(&G.qempty[q]);
         }
         busy += clk() - tb0;
+        if (elog && et == 0 && nelog < kChunkLog / 2) {   // chunklog rows [256, 512): per tile
+            unsigned long long* o = elog + 4 * (kChunkLog / 2 + nelog++);
+            o[0] = type; o[1] = e_loop - tb0; o[2] = e_ld; o[3] = clk() - e_bar;
+        }
         if (++q == kTaskRing) { q = 0; qphase ^= 1u; }
         if (++acc == kAccStages) { acc = 0; accphase ^= 1u; }
     }
@@ -1904,14 +1936,14 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
     } else if (warp == kWarpProducer) {
         if ((tid & 31) == 0) gemm_producer<PREC>(P, R, ring, G, trace);
     } else if (warp >= kWarpConv0 && warp < kWarpConv0 + 4) {
-        gemm_wconvert<PREC>(P, ring, G, trace,
-                            (cta == 0 && warp == kWarpConv0 && R.chunklog) ? R.chunklog : nullptr);
+        gemm_wconvert<PREC>(P, ring, G, trace, nullptr);
     } else if (warp < 4) {
-        if constexpr (PREC == kFP32) {
-            if (P.fused_combine) gemm_epilogue<PREC, true>(P, R, G, s_stat, trace);
-            else gemm_epilogue<PREC, false>(P, R, G, s_stat, trace);
+        unsigned long long* elog = (cta == 0 && R.chunklog) ? R.chunklog : nullptr;
+        if constexpr (PREC == kFP32) {   // bf16 keeps the combine phase (measured: fusing does not pay)
+            if (P.fused_combine) gemm_epilogue<PREC, true>(P, R, G, s_stat, trace, elog);
+            else gemm_epilogue<PREC, false>(P, R, G, s_stat, trace, elog);
         } else {
-            gemm_epilogue<PREC, false>(P, R, G, s_stat, trace);
+            gemm_epilogue<PREC, false>(P, R, G, s_stat, trace, elog);
         }
     }
     __syncthreads();
