@@ -1575,7 +1575,7 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
                               unsigned long long* trace, unsigned long long* elog) {
     int nelog = 0;
     long long w_acc = 0, busy = 0;
-    const int et = threadIdx.x;   // warps 0-3: 0..127 == TMEM lane == feature row in the tile
+    const int et = threadIdx.x - kWarpEpi0 * 32;   // 0..127 == TMEM lane == feature row in the tile
     const int wq = et >> 5;
     const uint32_t par = P.epoch & 1u;
     int q = 0;
@@ -1606,7 +1606,7 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
         const Task& tk = G.ring[q];   // stays valid until this warp group releases the slot
         const int type = tk.type;
         if (type < 0) {
-            if (threadIdx.x == 0) { trace[kWaitEpiAcc] = w_acc; trace[kEpiBusy] = busy; }
+            if (et == 0) { trace[kWaitEpiAcc] = w_acc; trace[kEpiBusy] = busy; }
             return;
         }
         if (!FD_TIMED_WAIT(w_acc, mbar_wait(&G.tfull[acc], accphase, P.abort_flag))) return;
@@ -1937,7 +1937,7 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
         if ((tid & 31) == 0) gemm_producer<PREC>(P, R, ring, G, trace);
     } else if (warp >= kWarpConv0 && warp < kWarpConv0 + 4) {
         gemm_wconvert<PREC>(P, ring, G, trace, nullptr);
-    } else if (warp < 4) {
+    } else if (warp >= kWarpEpi0 && warp < kWarpEpi0 + 4) {
         unsigned long long* elog = (cta == 0 && R.chunklog) ? R.chunklog : nullptr;
         if constexpr (PREC == kFP32) {   // bf16 keeps the combine phase (measured: fusing does not pay)
             if (P.fused_combine) gemm_epilogue<PREC, true>(P, R, G, s_stat, trace, elog);
@@ -2069,8 +2069,8 @@ __global__ void __launch_bounds__(kThreads, 1) debug_gemm_kernel(const __grid_co
         LaunchParams P{};
         P.H = K; P.D = K; P.abort_flag = abort_flag;
         gemm_wconvert<PREC>(P, smem, G, nullptr, nullptr);
-    } else if (warp < 4) {
-        const int et = tid, wq = et >> 5;
+    } else if (warp >= kWarpEpi0 && warp < kWarpEpi0 + 4) {
+        const int et = tid - kWarpEpi0 * 32, wq = et >> 5;
         mbar_wait(&G.tfull[0], 0, abort_flag);
         tc_fence_after();
         for (int ch = 0; ch < kNT / 32; ++ch) {
