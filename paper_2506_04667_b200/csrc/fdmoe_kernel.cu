@@ -1516,6 +1516,10 @@ __device__ void gemm_mma(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, unsi
     int acc = 0;
     uint32_t accphase = 0;
     const uint32_t tmem = G.tmem_base;
+    // per-stage constants of the 2-stage ring, hoisted out of the tile loop (lean path below)
+    const uint32_t abase_s[2] = {tmem + Cfg::TMEM_A0, tmem + Cfg::TMEM_A0 + Cfg::A_COLS};
+    const uint64_t bdesc_s[2] = {umma_desc_kmajor(smem_u32(ring), 128),
+                                 umma_desc_kmajor(smem_u32(ring + Cfg::STAGE_BYTES), 128)};
     while (true) {
         if (!FD_TIMED_WAIT(w_task, mbar_wait(&G.qfull[q], qphase, P.abort_flag))) return;
         const int type = G.ring[q].type;
@@ -1533,6 +1537,31 @@ __device__ void gemm_mma(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, unsi
         long long t_rdy = chunklog ? clk() : 0;
         if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.ready[stage], phase, P.abort_flag))) return;
         tc_fence_after();
+        if (Cfg::STAGES == 2 && stage == 0 && (nk & 1) == 0 && !chunklog) {
+            // Lean path (tile starts at ring slot 0, even stage count): stage pairs with compile-time
+            // slot indices, so a stage boundary is the commit, one probe and the descriptor selects.
+            for (int kb = 0; kb < nk; kb += 2) {
+                const bool last = kb + 2 == nk;
+                issue_stage<PREC, 0, kProbeAt>(d_tmem, abase_s[0], bdesc_s[0], kb == 0);
+                const bool r1 = mbar_test_wait(&G.ready[1], phase);
+                issue_stage<PREC, kProbeAt, NM>(d_tmem, abase_s[0], bdesc_s[0], kb == 0);
+                mma_commit(&G.done[0]);
+                if (!r1 && !FD_TIMED_WAIT(w_x, mbar_wait(&G.ready[1], phase, P.abort_flag))) return;
+                tc_fence_after();
+                issue_stage<PREC, 0, kProbeAt>(d_tmem, abase_s[1], bdesc_s[1], 0u);
+                const bool r0 = last || mbar_test_wait(&G.ready[0], phase ^ 1u);
+                issue_stage<PREC, kProbeAt, NM>(d_tmem, abase_s[1], bdesc_s[1], 0u);
+                mma_commit(&G.done[1]);
+                phase ^= 1u;
+                if (!last) {
+                    if (!r0 && !FD_TIMED_WAIT(w_x, mbar_wait(&G.ready[0], phase, P.abort_flag))) return;
+                    tc_fence_after();
+                }
+            }
+            mma_commit(&G.tfull[acc]);
+            if (++acc == kAccStages) { acc = 0; accphase ^= 1u; }
+            continue;
+        }
 #pragma unroll 4   // fewer loop back-edges (and their YIELDs) between stages (measured: 4 beats 1/2/8/16)
         for (int kb = 0; kb < nk; ++kb) {
             const long long t_iss = chunklog ? clk() : 0;
