@@ -1599,6 +1599,26 @@ __device__ void gemm_mma(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, unsi
 }
 
 // warps 8-11: thread = output feature (TMEM lane), 32 token columns per tcgen05.ld
+// GEMM0 epilogue of one 32-token chunk: +b1, activation, store C1 (tf32 hi/lo planes or bf16).
+// Row i of the chunk lives at +i*D; bit i of vmask = row holds a landed token (warp-uniform).
+template <int PREC, int ACT>
+__device__ __forceinline__ void epi_gemm0(const uint32_t (&r)[32], uint32_t vmask, float bias, float* hi, float* lo,
+                                          __nv_bfloat16* bf, int D) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        if (!(vmask & (1u << i))) continue;
+        const float v = activation(ACT, __fadd_rn(__uint_as_float(r[i]), bias));
+        const size_t o = (size_t)i * D;
+        if (PREC == kFP32) {
+            const float h = tf32_hi(v);
+            hi[o] = h;
+            lo[o] = __fsub_rn(v, h);
+        } else {
+            bf[o] = __float2bfloat16_rn(v);
+        }
+    }
+}
+
 template <int PREC, bool FUSED>
 __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl& G, unsigned long long* stat,
                               unsigned long long* trace, unsigned long long* elog) {
@@ -1707,22 +1727,20 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
             tmem_wait_ld();
             e_ld += clk() - tl0;
             if (!fvalid || (P.debug & kDbgNoEpiStore)) vmask = 0;
+            // separate compact loops per tile type and activation (one fully unrolled body with every
+            // variant inlined — erff included — was ~20 KB of SASS streamed through the I-cache per chunk)
+            if (type == 0) {
+                float* hi = c1hi + (size_t)ch * 32 * P.D;
+                float* lo = c1lo + (size_t)ch * 32 * P.D;
+                __nv_bfloat16* bf = c1b + (size_t)ch * 32 * P.D;
+                if (P.act == 0) epi_gemm0<PREC, 0>(r, vmask, bias, hi, lo, bf, P.D);
+                else if (P.act == 1) epi_gemm0<PREC, 1>(r, vmask, bias, hi, lo, bf, P.D);
+                else epi_gemm0<PREC, 2>(r, vmask, bias, hi, lo, bf, P.D);
+            } else {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                if (!(vmask & (1u << i))) continue;   // warp-uniform: same token row for all lanes
-                const int n = ch * 32 + i;
-                float v = __fadd_rn(__uint_as_float(r[i]), bias);
-                if (type == 0) {
-                    v = activation(P.act, v);
-                    const size_t o = (size_t)n * P.D;
-                    if (PREC == kFP32) {
-                        const float h = tf32_hi(v);
-                        c1hi[o] = h;
-                        c1lo[o] = __fsub_rn(v, h);
-                    } else {
-                        c1b[o] = __float2bfloat16_rn(v);
-                    }
-                } else {
+                for (int i = 0; i < 32; ++i) {
+                    if (!(vmask & (1u << i))) continue;   // warp-uniform: same token row for all lanes
+                    const float v = __fadd_rn(__uint_as_float(r[i]), bias);
                     // row n's pointer (and weight) from lane i of this chunk's prefetch
                     float* rp = reinterpret_cast<float*>(
                         __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(rowp[ch]), i));
