@@ -13,7 +13,7 @@ namespace fdmoe {
 // allocator, w10 tile scheduler + TMA producer, w11 tcgen05.mma issuer (the warp arbiter favours
 // high warp ids, so the single-lane issuers sit on top).
 constexpr int kThreads = 384;
-constexpr int kWarpEpi0 = 4, kWarpConv0 = 0, kWarpTmem = 8, kWarpProducer = 10, kWarpMma = 11;
+constexpr int kWarpEpi0 = 4, kWarpConv0 = 0, kWarpTmem = 8, kWarpSignal = 9, kWarpProducer = 10, kWarpMma = 11;
 constexpr int kBM = 128;            // tokens per row tile of an expert's receive region
 constexpr int kBF = 128;            // output features per FFN tile (MMA M = TMEM lanes)
 constexpr int kNT = 128;            // tokens per FFN tile (MMA N = accumulator columns)

@@ -1212,10 +1212,13 @@ struct GemmCtrl {
     uint64_t wfull[8], wempty[8];                    // weight smem ring (producer -> converters)
     uint64_t tfull[kAccStages], tempty[kAccStages];  // accumulators
     uint64_t qfull[kTaskRing], qempty[kTaskRing];    // task ring
+    uint64_t sfull[kTaskRing], sempty[kTaskRing];    // epilogue -> signal warp (finished tiles)
     uint32_t tmem_base;
     uint32_t pad;
     Task ring[kTaskRing];
+    Task sring[kTaskRing];                           // finished tiles awaiting their release signals
 };
+static_assert(sizeof(GemmCtrl) <= 1024, "GemmCtrl fits the control area");
 constexpr int kTaskConsumers = 1 + 4 + 1;   // MMA warp, 4 converter warps, epilogue
 constexpr int kReadyCount = 1 + 4;          // producer (expect_tx) + 4 converter warps
 
@@ -1599,6 +1602,51 @@ __device__ void gemm_mma(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, unsi
 }
 
 // warps 8-11: thread = output feature (TMEM lane), 32 token columns per tcgen05.ld
+// warp 9, one lane: release signals of finished tiles, in tile order (runtime.hpp:685-690). Every
+// epilogue thread's stores precede the hand-off (bar.sync, then the mbarrier arrive/wait pair), so the
+// fence here orders them before the counter / flag release (cumulativity).
+__device__ void gemm_signal(const LaunchParams& P, const RankCtx& R, GemmCtrl& G, unsigned long long* stat) {
+    const uint32_t par = P.epoch & 1u;
+    const int cta = blockIdx.x % P.ctas_per_rank;
+    const int e_glob_base = R.rank * P.El;
+    int sq = 0;
+    uint32_t sphase = 0;
+    while (true) {
+        if (!mbar_wait(&G.sfull[sq], sphase, P.abort_flag)) return;
+        const Task tk = G.sring[sq];
+        mbar_arrive(&G.sempty[sq]);
+        if (++sq == kTaskRing) { sq = 0; sphase ^= 1u; }
+        if (tk.type < 0) return;
+        int rows = 0;
+        for (int j = 0; j < tk.nsrc; ++j) rows += tk.cnt[j];
+        if (tk.type == 0) {
+            __threadfence();
+            // event before the counter release: GEMM0's end precedes any dependent GEMM1 start
+            emit_event(P, R, kEvExec, cta, kTaskGemm0, tk.t0, globaltimer(), tk.src0, tk.le, tk.m, tk.nb,
+                       tk.nsrc, rows);
+            atomicAdd(R.g0done + (size_t)tk.le * P.MT + tk.m, 1u);
+            stat[0]++;
+        } else {
+            // the tile's rows went to the origin rank: system scope when it may be another GPU
+            if (P.nranks == P.P) __threadfence(); else __threadfence_system();
+            emit_event(P, R, kEvExec, cta, kTaskGemm1, tk.t0, globaltimer(), tk.src0, tk.le, tk.m, tk.nb,
+                       tk.nsrc, rows);
+            const int e_glob = e_glob_base + tk.le;
+            const int rbf = P.Cp >= kBM ? (tk.m % (P.Cp / kBM)) : 0;
+            for (int j = 0; j < tk.nsrc && !P.fused_combine; ++j) {
+                if (tk.cnt[j] <= 0) continue;
+                unsigned long long* f = reinterpret_cast<unsigned long long*>(R.peer_heap[tk.src0 + j] +
+                                                                              R.hl.cflag[par]) +
+                                        ((size_t)e_glob * P.RBF + rbf) * P.NB1 + tk.nb;
+                emit_event(P, R, kEvTilePut, cta, kTaskGemm1, globaltimer(), 0, R.rank, tk.le, tk.m, tk.nb,
+                           tk.src0 + j, tk.cnt[j]);
+                st_release_sys(f, ((uint64_t)P.epoch << 32) | (uint32_t)tk.cnt[j]);
+            }
+            stat[1]++;
+        }
+    }
+}
+
 // GEMM0 epilogue of one 32-token chunk: +b1, activation, store C1 (tf32 hi/lo planes or bf16).
 // Row i of the chunk lives at +i*D; bit i of vmask = row holds a landed token (warp-uniform).
 template <int PREC, int ACT>
@@ -1633,6 +1681,8 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
     uint32_t accphase = 0;
     const uint32_t tmem = G.tmem_base;
     const int e_glob_base = R.rank * P.El;
+    int sq = 0;
+    uint32_t sphase = 0;
     bool zero_seen = false;
     if (FUSED) {
         // fused combine accumulates into the output: zero this CTA's token rows while the first tile's
@@ -1655,7 +1705,13 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
         const Task& tk = G.ring[q];   // stays valid until this warp group releases the slot
         const int type = tk.type;
         if (type < 0) {
-            if (et == 0) { trace[kWaitEpiAcc] = w_acc; trace[kEpiBusy] = busy; }
+            if (et == 0) {
+                trace[kWaitEpiAcc] = w_acc; trace[kEpiBusy] = busy;
+                if (mbar_wait(&G.sempty[sq], sphase ^ 1u, P.abort_flag)) {   // end marker for the signal warp
+                    G.sring[sq].type = -1;
+                    mbar_arrive(&G.sfull[sq]);
+                }
+            }
             return;
         }
         if (!FD_TIMED_WAIT(w_acc, mbar_wait(&G.tfull[acc], accphase, P.abort_flag))) return;
@@ -1761,33 +1817,12 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
         e_bar = clk();
         if (et == 0) {
             mbar_arrive(&G.tempty[acc]);
-            int rows = 0;
-            for (int j = 0; j < tk.nsrc; ++j) rows += tk.cnt[j];
-            if (type == 0) {
-                __threadfence();
-                // event before the counter release: GEMM0's end precedes any dependent GEMM1 start
-                emit_event(P, R, kEvExec, blockIdx.x % P.ctas_per_rank, kTaskGemm0, tk.t0, globaltimer(), tk.src0,
-                           tk.le, tk.m, tk.nb, tk.nsrc, rows);
-                atomicAdd(R.g0done + (size_t)tk.le * P.MT + tk.m, 1u);
-                stat[0]++;
-            } else {
-                // the tile's rows went to the origin rank: system scope when it may be another GPU
-                if (P.nranks == P.P) __threadfence(); else __threadfence_system();
-                const int cta = blockIdx.x % P.ctas_per_rank;
-                emit_event(P, R, kEvExec, cta, kTaskGemm1, tk.t0, globaltimer(), tk.src0, tk.le, tk.m, tk.nb,
-                           tk.nsrc, rows);
-                const int rbf = P.Cp >= kBM ? (tk.m % (P.Cp / kBM)) : 0;
-                for (int j = 0; j < tk.nsrc && !FUSED; ++j) {
-                    if (tk.cnt[j] <= 0) continue;
-                    unsigned long long* f = reinterpret_cast<unsigned long long*>(R.peer_heap[tk.src0 + j] +
-                                                                                  R.hl.cflag[par]) +
-                                            ((size_t)e_glob * P.RBF + rbf) * P.NB1 + tk.nb;
-                    emit_event(P, R, kEvTilePut, cta, kTaskGemm1, globaltimer(), 0, R.rank, tk.le, tk.m, tk.nb,
-                               tk.src0 + j, tk.cnt[j]);
-                    st_release_sys(f, ((uint64_t)P.epoch << 32) | (uint32_t)tk.cnt[j]);
-                }
-                stat[1]++;
-            }
+            // the tile's release signals (fence + counters / flags) go to the signal warp: the epilogue
+            // moves on to the next accumulator instead of waiting out the fence
+            if (!mbar_wait(&G.sempty[sq], sphase ^ 1u, P.abort_flag)) return;
+            G.sring[sq] = tk;
+            mbar_arrive(&G.sfull[sq]);
+            if (++sq == kTaskRing) { sq = 0; sphase ^= 1u; }
             mbar_arrive(&G.qempty[q]);
         }
         busy += clk() - tb0;
@@ -1971,6 +2006,7 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
         for (int i = 0; i < Cfg::WSTAGES; ++i) { mbar_init(&G.wfull[i], 1); mbar_init(&G.wempty[i], 4); }
         for (int i = 0; i < kAccStages; ++i) { mbar_init(&G.tfull[i], 1); mbar_init(&G.tempty[i], 1); }
         for (int i = 0; i < kTaskRing; ++i) { mbar_init(&G.qfull[i], 1); mbar_init(&G.qempty[i], kTaskConsumers); }
+        for (int i = 0; i < kTaskRing; ++i) { mbar_init(&G.sfull[i], 1); mbar_init(&G.sempty[i], 1); }
         G.tmem_base = tmem_base;
         mbar_fence_init();
     }
@@ -1984,6 +2020,8 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
         if ((tid & 31) == 0) gemm_producer<PREC>(P, R, ring, G, trace);
     } else if (warp >= kWarpConv0 && warp < kWarpConv0 + 4) {
         gemm_wconvert<PREC>(P, ring, G, trace, nullptr);
+    } else if (warp == kWarpSignal) {
+        if ((tid & 31) == 0) gemm_signal(P, R, G, s_stat);
     } else if (warp >= kWarpEpi0 && warp < kWarpEpi0 + 4) {
         unsigned long long* elog = (cta == 0 && R.chunklog) ? R.chunklog : nullptr;
         if constexpr (PREC == kFP32) {   // bf16 keeps the combine phase (measured: fusing does not pay)
