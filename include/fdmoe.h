@@ -231,7 +231,7 @@ fdmoe_status fdmoe_get_info(fdmoe_handle* h, fdmoe_info* info);
  * max over this handle's devices). Call after fdmoe_sync / fdmoe_forward. */
 fdmoe_status fdmoe_last_kernel_ms(fdmoe_handle* h, double* ms);
 /* Device trace of the most recent launch (the reference's TraceBuffer role, trace.hpp:17-118, at
- * phase granularity): per CTA of local rank `local_rank`, 24 u64 = %globaltimer ns at kernel start,
+ * phase granularity): per CTA of local rank `local_rank`, 28 u64 = %globaltimer ns at kernel start,
  * gate done, grid barrier passed, dispatch done, FFN tiles done, combine done, exit; the number of
  * FFN tiles that CTA executed; then SM cycles blocked per FFN pipeline edge: MMA<-tokens,
  * MMA<-weights, MMA<-accumulator, converter<-weight TMA, converter<-TMEM stage, producer<-weight

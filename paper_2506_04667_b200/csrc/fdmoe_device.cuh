@@ -28,14 +28,15 @@ constexpr int kMaxRanks = 64;       // P envelope (peer table size)
 constexpr int kMaxSrcPerTile = 8;   // packet_rows >= 16 -> <= 8 packets per 128-row tile
 constexpr int kCombineTok = 16;     // tokens per combine task (== kGateTok)
 constexpr int kMaxLocalRanks = 8;   // ranks per launch (virtual ranks on one GPU)
-constexpr int kTracePts = 24;
+constexpr int kTracePts = 28;
 constexpr int kGroupBarriers = 2;   // sequential mode: after dispatch, after the expert FFN
 constexpr int kChunkLog = 512;       // start, gate, barrier, dispatch, gemm, combine, end, tiles,
                                     // then FFN pipeline wait cycles (see kWait*)
 enum WaitSlot : int {
     kWaitMmaX = 8, kWaitMmaA, kWaitMmaAcc, kWaitConvW, kWaitConvA, kWaitProdW, kWaitProdX, kWaitEpiAcc,
     kWaitMmaTask, kProdFetch, kEpiBusy, kMmaTiles,
-    kTrPrefix = 20, kTrSlots, kTrSlotBarrier, kTrPush   // dispatch sub-phases (%globaltimer)
+    kTrPrefix = 20, kTrSlots, kTrSlotBarrier, kTrPush,   // dispatch sub-phases (%globaltimer)
+    kTrGateLogits = 24, kTrGatePairs, kTrGateFull, kTrGateNFull   // gate sub-phases (last sub-tile), full tokens
 };
 
 enum Prec : int { kFP32 = 0, kBF16 = 1 };

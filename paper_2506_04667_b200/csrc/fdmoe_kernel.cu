@@ -887,6 +887,7 @@ __device__ void gate_phase(const LaunchParams& P, const RankCtx& R, const float*
             if (r == 2 && (tid & 31) == 0) g.sFull[atomicAdd(&s_nfull, 1)] = tokA + s0 + t;
         }
         __syncthreads();
+        if (tid == 0) R.trace[(size_t)cta * kTracePts + kTrGateLogits] = globaltimer();
         const int np = min(s_np, kGatePairCap);
         if (np > 0 && !(P.debug & kDbgGateNoFlush)) {
             gate_pairs_exact(P, R, A, g, np);
@@ -898,6 +899,7 @@ __device__ void gate_phase(const LaunchParams& P, const RankCtx& R, const float*
             }
             __syncthreads();
         }
+        if (tid == 0) R.trace[(size_t)cta * kTracePts + kTrGatePairs] = globaltimer();
         const int nf = s_nfull;
         if (nf > 0 && !(P.debug & kDbgGateNoFlush)) {   // ties / near-ties / overflow: the reference chain for all E
             gate_full_exact(P, R, A, g, nf);
@@ -906,7 +908,11 @@ __device__ void gate_phase(const LaunchParams& P, const RankCtx& R, const float*
         }
         __syncthreads();
     }
-    if (tid == 0) { stat[3] += n_full; }
+    if (tid == 0) {
+        stat[3] += n_full;
+        R.trace[(size_t)cta * kTracePts + kTrGateFull] = globaltimer();
+        R.trace[(size_t)cta * kTracePts + kTrGateNFull] = n_full;
+    }
     if ((tid & 31) == 0 && n_pair_tok) atomicAdd(&stat[4], n_pair_tok);
     __syncthreads();
     for (int e = tid; e < E; e += kThreads) R.cnt_cta[(size_t)cta * E + e] = g.sCnt[e];

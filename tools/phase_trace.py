@@ -19,6 +19,11 @@ for i, n in enumerate(names):
     print(f"{n:9s} min {t[:, i].min():9.1f}  med {np.median(t[:, i]):9.1f}  max {t[:, i].max():9.1f} us")
 for i, n in ((20, "prefix"), (21, "slots"), (22, "slot-barrier"), (23, "push")):
     print(f"{n:12s} min {t[:, i].min():9.1f}  med {np.median(t[:, i]):9.1f}  max {t[:, i].max():9.1f} us")
+g = t[:, 1]
+worst = int(np.argmax(g))
+print(f"slowest gate CTA {worst}: logits {t[worst, 24]/1:.1f} pairs {t[worst, 25]:.1f} full {t[worst, 26]:.1f} us "
+      f"(full-exact tokens {int(round(t[worst, 27] * 1e3))}); median CTA: logits {np.median(t[:, 24]):.1f} "
+      f"pairs {np.median(t[:, 25]):.1f} full {np.median(t[:, 26]):.1f}")
 print("ffn tiles per CTA: min", int(t[:, 7].min()), "max", int(t[:, 7].max()), "sum", int(t[:, 7].sum()))
 ffn_cyc = (t[:, 4] - t[:, 3]).mean() * 1e3 * 1.965   # ns -> cycles at max clock (approx)
 for i, n in enumerate(["mma<-tokens", "mma<-weights", "mma<-acc", "conv<-wTMA", "conv<-tmemA", "prod<-wslot", "prod<-xslot", "epi<-acc"]):
