@@ -394,10 +394,11 @@ __device__ void gate_logits(const LaunchParams& P, const RankCtx& R, const float
             if (st < nk) load_stage(st, st); else cp_async_commit();
         for (int kb = 0; kb < nk; ++kb) {
             const int st = kb % kGateStages;
+            cp_async_wait<kGateStages - 2>();   // chunk kb landed (kb + 1 may still be in flight)
+            __syncthreads();                     // ... for every thread, and everyone is past chunk kb - 1,
+            // so its slot takes chunk kb + 2 now: one barrier per chunk instead of two
             if (kb + kGateStages - 1 < nk) load_stage((kb + kGateStages - 1) % kGateStages, kb + kGateStages - 1);
             else cp_async_commit();
-            cp_async_wait<kGateStages - 1>();
-            __syncthreads();
             const float* a = g.sA + st * g.sub * kGateApitch;
             const float* w = g.sW + st * kGateKC * Ep;
             if (FAST && tid < ts && !(P.debug & kDbgGateNoNorm)) {   // |a|^2: 32-term float chunks, double sum
@@ -441,7 +442,6 @@ __device__ void gate_logits(const LaunchParams& P, const RankCtx& R, const float
                     }
                 }
             }
-            __syncthreads();   // stage st may be refilled next iteration
         }
         cp_async_wait<0>();
         if (active) {
