@@ -1847,7 +1847,7 @@ static_assert(kCombineTok == kGateTok, "combine tasks are aligned with gate bloc
 // per token, 16-byte column chunks, all of a token's landed rows loaded before the adds.
 // The CTA first waits once for every combine tile this rank expects (n_e = kept rows per expert,
 // saved from the dispatch phase in sN), so the per-token loop has no flag traffic.
-constexpr int kCombUnroll = 4;
+constexpr int kCombUnroll = 8;
 
 __device__ void combine_phase(const LaunchParams& P, const RankCtx& R, float* __restrict__ O, uint8_t* smem,
                               const int* __restrict__ sN, unsigned long long* stat) {
