@@ -8,10 +8,12 @@
 namespace fdmoe {
 
 // ---------------------------------------------------------------- constants
-// 12 warps. FFN roles: w0-3 epilogue (TMEM -> registers -> bias/activation -> global / peer
-// stores), w4-7 weight converters (TMA-staged smem -> registers -> tf32 hi/lo -> TMEM), w8 TMEM
-// allocator, w10 tile scheduler + TMA producer, w11 tcgen05.mma issuer (the warp arbiter favours
-// high warp ids, so the single-lane issuers sit on top).
+// 12 warps. FFN roles: w0-3 weight converters (TMA-staged smem -> registers -> tf32 hi/lo -> TMEM),
+// w4-7 epilogue (TMEM -> registers -> bias/activation -> global / peer stores), w8 TMEM allocator,
+// w9 signal warp (tile release fences / counters / flags), w10 tile scheduler + TMA producer, w11
+// tcgen05.mma issuer (the warp arbiter favours high warp ids, so the single-lane issuers sit on top
+// and the epilogue above the converters). A warp reaches TMEM lanes 32*(warp % 4) .. +31 only, so
+// each 4-warp group covers all 128 lanes.
 constexpr int kThreads = 384;
 constexpr int kWarpEpi0 = 4, kWarpConv0 = 0, kWarpTmem = 8, kWarpSignal = 9, kWarpProducer = 10, kWarpMma = 11;
 constexpr int kBM = 128;            // tokens per row tile of an expert's receive region

@@ -13,9 +13,10 @@
 //                        last CTA to finish a packet publishes a release.sys signal
 //                        carrying the row count (zero-row packets signal too,
 //                        runtime.hpp:328-331)
-//   3. expert FFN        tile queue (one atomic head per rank): warp 0 waits for the
+//   3. expert FFN        tile queue (one atomic head per rank): warp 10 waits for the
 //                        packet signals / GEMM0 row-tile counters, then TMA-streams
-//                        operands into a smem ring; warp 1 issues tcgen05.mma into
+//                        operands into a smem ring; warps 0-3 split the weights into
+//                        tf32 hi/lo TMEM operands; warp 11 issues tcgen05.mma into
 //                        double-buffered TMEM accumulators; warps 4-7 drain TMEM:
 //                        GEMM0 epilogue = +b1, activation, split -> C1 scratch;
 //                        GEMM1 epilogue = +b2, rows stored directly into the ORIGIN
@@ -1282,7 +1283,7 @@ __device__ int resolve_tile_rows(const LaunchParams& P, const RankCtx& R, Task& 
         _ok;                                  \
     })
 
-// warp 0, one lane: fetch tiles, resolve dependencies, stream the token operand
+// warp 10, one lane: fetch tiles, resolve dependencies, stream both operands
 template <int PREC>
 __device__ void gemm_producer(const LaunchParams& P, const RankCtx& R, uint8_t* ring, GemmCtrl& G,
                               unsigned long long* trace) {
@@ -1371,7 +1372,7 @@ __device__ void gemm_producer(const LaunchParams& P, const RankCtx& R, uint8_t* 
     }
 }
 
-// warps 4-7: weight tile (TMA-staged in smem, SWIZZLE_128B) -> registers -> tf32 hi/lo split ->
+// warps 0-3: weight tile (TMA-staged in smem, SWIZZLE_128B) -> registers -> tf32 hi/lo split ->
 // tcgen05.st into the TMEM weight ring. Thread (warp 4+q, lane l) owns feature row r = 32q+l of
 // the tile = TMEM lane r; in atom a its 16-byte chunk c sits at a*16K + r*128 + ((c ^ (r & 7)) << 4),
 // so a warp's 128-bit loads are bank-conflict free.
@@ -1607,7 +1608,7 @@ __device__ void gemm_mma(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, unsi
     }
 }
 
-// warps 8-11: thread = output feature (TMEM lane), 32 token columns per tcgen05.ld
+// warps 4-7: thread = output feature (TMEM lane), 32 token columns per tcgen05.ld
 // warp 9, one lane: release signals of finished tiles, in tile order (runtime.hpp:685-690). Every
 // epilogue thread's stores precede the hand-off (bar.sync, then the mbarrier arrive/wait pair), so the
 // fence here orders them before the counter / flag release (cumulativity).
