@@ -1302,6 +1302,10 @@ __device__ void gemm_producer(const LaunchParams& P, const RankCtx& R, uint8_t* 
     }
     tma_prefetch(&R.tm_w1);
     tma_prefetch(&R.tm_w2);
+    // weights stream through once (evict first); token / C1 tiles are re-read by the other feature
+    // blocks of the same row tile (keep)
+    const uint64_t pol_w = l2_policy_evict_first();
+    const uint64_t pol_x = l2_policy_evict_last();
     while (true) {
         const long long tf0 = clk();
         const uint32_t t = atomicAdd(R.gemm_head, 1u);
@@ -1350,8 +1354,8 @@ __device__ void gemm_producer(const LaunchParams& P, const RankCtx& R, uint8_t* 
                 mbar_expect_tx(&G.wfull[wstage], Cfg::W_BYTES);
 #pragma unroll
                 for (int at = 0; at < Cfg::NATOM; ++at)
-                    tma_load_2d(ring + Cfg::W_OFF + wstage * Cfg::W_BYTES + at * Cfg::ATOM_BYTES, tw,
-                                &G.wfull[wstage], kb * Cfg::BK + at * Cfg::ATOM_K, yw);
+                    tma_load_2d_hint(ring + Cfg::W_OFF + wstage * Cfg::W_BYTES + at * Cfg::ATOM_BYTES, tw,
+                                     &G.wfull[wstage], kb * Cfg::BK + at * Cfg::ATOM_K, yw, pol_w);
             }
             if (++wstage == Cfg::WSTAGES) { wstage = 0; wphase ^= 1u; }
 
@@ -1364,8 +1368,8 @@ __device__ void gemm_producer(const LaunchParams& P, const RankCtx& R, uint8_t* 
                 for (int pl = 0; pl < Cfg::PLANES; ++pl)
 #pragma unroll
                     for (int at = 0; at < Cfg::NATOM; ++at)
-                        tma_load_2d(st + pl * Cfg::PLANE_BYTES + at * Cfg::ATOM_BYTES, tb[pl], &G.ready[stage],
-                                    kb * Cfg::BK + at * Cfg::ATOM_K, y);
+                        tma_load_2d_hint(st + pl * Cfg::PLANE_BYTES + at * Cfg::ATOM_BYTES, tb[pl], &G.ready[stage],
+                                         kb * Cfg::BK + at * Cfg::ATOM_K, y, pol_x);
             }
             if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
         }
