@@ -296,6 +296,12 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool vali
                  "r"(valid ? 16 : 0)
                  : "memory");
 }
+// same, with an L2 cache-policy hint (the gate's token rows are read again by the row push ~100 us later)
+__device__ __forceinline__ void cp_async16_hint(void* dst, const void* src, uint64_t policy) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+                 "l"(policy)
+                 : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -352,6 +358,7 @@ __device__ void gate_logits(const LaunchParams& P, const RankCtx& R, const float
     const int n_tg = (ts + TT - 1) / TT;
     const int n_items = n_tg * n_eg;
     const int nk = H / kGateKC;   // envelope: H % 32 == 0
+    const uint64_t pol_a = l2_policy_evict_last();   // token rows: keep for the dispatch push
     for (int base = 0; base < n_items; base += kThreads) {   // item rounds (re-stream K per round)
         auto load_stage = [&](int st, int kb) {
             if (P.debug & kDbgGateNoLoad) { cp_async_commit(); return; }
@@ -361,7 +368,7 @@ __device__ void gate_logits(const LaunchParams& P, const RankCtx& R, const float
             for (int i = tid; i < ts * 8; i += kThreads) {
                 const int t = i >> 3, c = i & 7;
                 const int tok = rows ? rows[t] : tok0 + t;
-                cp_async16(a + t * kGateApitch + c * 4, A + (size_t)tok * H + k0 + c * 4, true);
+                cp_async16_hint(a + t * kGateApitch + c * 4, A + (size_t)tok * H + k0 + c * 4, pol_a);
             }
             if (w_vec) {
                 const int cpr = Ep >> 2;
