@@ -110,24 +110,47 @@ def dist_env():
     return rank, world, local
 
 
-def cpu_reference(cfg_full, sample_tokens, steps, warmup, seed=0):
-    """The reference's own forward() (runtime.hpp:802) from oracle/_ref on a token sample of the same
-    workload (same H, I, E, k, cf; S reduced to the sample), every host core as processor threads."""
-    import paper_2506_04667_b200 as fd
+def _ref_cfg(cfg_full, tokens, seed=0):
+    """A plain config record for oracle/pyoracle (the reference arm never imports the product package)."""
+    from types import SimpleNamespace
+    return SimpleNamespace(tokens_per_device=tokens, embed_dim=cfg_full.embed_dim, ffn_dim=cfg_full.ffn_dim,
+                           experts_total=cfg_full.experts_total, devices=1, topk=cfg_full.topk,
+                           capacity_factor=cfg_full.capacity_factor, tile_rows=128, tile_cols=64, activation=0,
+                           seed=seed)
+
+
+_REF_MODELS = {}
+
+
+def _ref_runner(cfg):
+    """The reference's own forward() (runtime.hpp:802) from oracle/_ref with every host core as processor
+    threads, on inputs generated inside oracle/_ref by the reference harness's seeded generator
+    (harness.hpp:76-109); the oracle port (C restatement, threaded) when the reference was not built."""
     from oracle import pyoracle as po
     cores = os.cpu_count() or 1
-    cfg = fd.MoeConfig(tokens_per_device=sample_tokens, embed_dim=cfg_full.embed_dim, ffn_dim=cfg_full.ffn_dim,
-                       experts_total=cfg_full.experts_total, devices=1, topk=cfg_full.topk,
-                       capacity_factor=cfg_full.capacity_factor, tile_rows=128, tile_cols=64, seed=seed)
-    model = fd.make_model(cfg)
-    shards = fd.make_shards(cfg)
     if po.ref_available():
-        rm = po.RefModel(model, cfg)
-        run = lambda: po.ref_forward(cfg, shards, rm, processors=cores)  # noqa: E731
-        kind = "reference"
-    else:   # no prebuilt reference: the oracle port (C restatement), threaded
-        run = lambda: po.dense_forward(shards[0], model, cfg, threads=cores)  # noqa: E731
-        kind = "port"
+        key = (cfg.embed_dim, cfg.ffn_dim, cfg.experts_total, cfg.seed)
+        if key not in _REF_MODELS:   # the 4.3 GB c4 model is generated once per process
+            _REF_MODELS.clear()
+            _REF_MODELS[key] = po.RefModel(None, cfg)
+        rm = _REF_MODELS[key]
+        shards = po.ref_synth_shards(cfg)
+        return (lambda: po.ref_forward(cfg, shards, rm, processors=cores)), "reference", cores
+    from types import SimpleNamespace
+    rng = np.random.default_rng(cfg.seed)
+    H, D, E = cfg.embed_dim, cfg.ffn_dim, cfg.experts_total
+    f = lambda *sh: rng.standard_normal(sh, dtype=np.float32)  # noqa: E731
+    model = SimpleNamespace(wg=f(H, E) / np.sqrt(H), w1=f(E, H, D) / np.sqrt(H), b1=0.1 * f(E, D),
+                            w2=f(E, D, H) / np.sqrt(D), b2=0.1 * f(E, H))
+    shard = f(cfg.tokens_per_device, H)
+    return (lambda: po.dense_forward(shard, model, cfg, threads=cores)), "port", cores
+
+
+def cpu_reference(cfg_full, sample_tokens, steps, warmup, seed=0):
+    """The reference's CPU path on a token sample of the same workload (same H, I, E, k, cf; S reduced to
+    the sample)."""
+    cfg = _ref_cfg(cfg_full, sample_tokens, seed)
+    run, kind, cores = _ref_runner(cfg)
     for _ in range(warmup):
         run()
     t0 = time.perf_counter()
@@ -137,27 +160,15 @@ def cpu_reference(cfg_full, sample_tokens, steps, warmup, seed=0):
     return {"value": sample_tokens * steps / dt, "unit": "tokens/s", "cores": cores, "kind": kind,
             "sample": f"{sample_tokens} tokens x {steps} forward() calls of the same layer shape "
                       f"(H={cfg.embed_dim}, I={cfg.ffn_dim}, E={cfg.experts_total}, top-{cfg.topk}, cf=1, P=1)",
-            "ms_per_step": dt * 1e3 / steps}
+            "sample_tokens": sample_tokens, "ms_per_step": dt * 1e3 / steps}
 
 
 def calibrate_sample(cfg_full, budget_s):
     """Token sample size whose reference forward() takes about budget_s seconds on this host."""
-    from oracle import pyoracle as po
-    import paper_2506_04667_b200 as fd
     probe = 256
-    cfg = fd.MoeConfig(tokens_per_device=probe, embed_dim=cfg_full.embed_dim, ffn_dim=cfg_full.ffn_dim,
-                       experts_total=cfg_full.experts_total, devices=1, topk=cfg_full.topk, tile_rows=128,
-                       tile_cols=64)
-    model = fd.make_model(cfg)
-    shards = fd.make_shards(cfg)
-    cores = os.cpu_count() or 1
-    if po.ref_available():
-        rm = po.RefModel(model, cfg)
-        t0 = time.perf_counter()
-        po.ref_forward(cfg, shards, rm, processors=cores)
-    else:
-        t0 = time.perf_counter()
-        po.dense_forward(shards[0], model, cfg, threads=cores)
+    run, _, _ = _ref_runner(_ref_cfg(cfg_full, probe))
+    t0 = time.perf_counter()
+    run()
     dt = time.perf_counter() - t0
     n = int(probe * budget_s / max(dt, 1e-3))
     return max(128, min(S_PER_GPU, (n // 128) * 128))
@@ -182,28 +193,32 @@ def main():
         print(f"warning: WORLD_SIZE={world} != --gpus {args.gpus}; using WORLD_SIZE", file=sys.stderr)
     n = world if world > 1 else args.gpus
 
-    import paper_2506_04667_b200 as fd
-    prec = fd.Precision.fp32 if args.precision == "fp32" else fd.Precision.bf16
-    cfg = fd.MoeConfig(tokens_per_device=args.tokens, embed_dim=H, ffn_dim=D, experts_total=args.experts,
-                       devices=n, topk=TOPK, capacity_factor=1.0, tile_rows=128, tile_cols=64, seed=0,
-                       precision=prec)
-    workload = (f"c4-shape: T={cfg.tokens_per_device} tokens/GPU, H={H}, I={D}, E={cfg.experts_total} total "
-                f"({cfg.experts_total // n}/GPU), top-{TOPK}, cf=1.0, relu, EP={n}, "
-                f"{'FP32-accurate 3xTF32' if prec == 0 else 'bf16'}")
-    config = {"workload": workload, "tokens_per_gpu": cfg.tokens_per_device, "embed_dim": H, "ffn_dim": D,
-              "experts_total": cfg.experts_total, "topk": TOPK, "ep": n,
+    from types import SimpleNamespace
+    prec_fp32 = args.precision == "fp32"
+    shape = SimpleNamespace(tokens_per_device=args.tokens, embed_dim=H, ffn_dim=D, experts_total=args.experts,
+                            topk=TOPK, capacity_factor=1.0)
+    workload = (f"c4-shape: T={shape.tokens_per_device} tokens/GPU, H={H}, I={D}, E={shape.experts_total} total "
+                f"({shape.experts_total // n}/GPU), top-{TOPK}, cf=1.0, relu, EP={n}, "
+                f"{'FP32-accurate 3xTF32' if prec_fp32 else 'bf16'}")
+    config = {"workload": workload, "tokens_per_gpu": shape.tokens_per_device, "embed_dim": H, "ffn_dim": D,
+              "experts_total": shape.experts_total, "topk": TOPK, "ep": n,
               "l2": "no flush: per-step inputs (134 MB shard + resident expert weights) exceed the 126 MB L2"}
 
     # ---------------------------------------------------------------- reference arm
+    # The reference's own CPU forward() from oracle/_ref only: this branch never imports the product
+    # package (inputs come from the reference harness's generator inside oracle/_ref).
     if args.impl == "reference":
         if rank != 0:
             return
         budget = max(2.0, 150.0 / (args.steps + args.warmup))
-        sample = calibrate_sample(cfg, budget)
-        cb = cpu_reference(cfg, sample, args.steps, args.warmup)
+        sample = calibrate_sample(shape, budget)
+        cb = cpu_reference(shape, sample, args.steps, args.warmup)
+        ref_config = dict(config, sample_tokens=sample,
+                          sample_note=f"each step is the reference forward() on a {sample}-token sample of this "
+                                      f"workload (same H, I, E, k, cf); tokens/s = sample tokens / step time")
         line = {"metric": METRIC, "value": cb["value"], "unit": "tokens/s", "n_gpus": 0, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": cb["ms_per_step"], "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": ref_config,
                 "impl": "reference",
                 "cpu_baseline": {"value": cb["value"], "unit": "tokens/s", "cores": cb["cores"], "kind": cb["kind"],
                                  "sample": cb["sample"]},
@@ -212,6 +227,11 @@ def main():
         return
 
     # ---------------------------------------------------------------- our arm
+    import paper_2506_04667_b200 as fd
+    prec = fd.Precision.fp32 if prec_fp32 else fd.Precision.bf16
+    cfg = fd.MoeConfig(tokens_per_device=args.tokens, embed_dim=H, ffn_dim=D, experts_total=args.experts,
+                       devices=n, topk=TOPK, capacity_factor=1.0, tile_rows=128, tile_cols=64, seed=0,
+                       precision=prec)
     import torch
     import torch.distributed as dist
     torch.cuda.set_device(local)
@@ -378,9 +398,9 @@ def main():
     if rank == 0 and not args.no_cpu_baseline:
         try:
             budget = 15.0
-            sample = calibrate_sample(cfg, budget)
-            cb = cpu_reference(cfg, sample, 1, 0)
-            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            sample = calibrate_sample(shape, budget)
+            cb = cpu_reference(shape, sample, 1, 0)
+            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "sample_tokens")}
         except Exception as e:  # never let the baseline break the bench line
             line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
     if rank == 0:

@@ -199,15 +199,18 @@ typedef struct {
     const float* weights;   /* S x k */
     float* out;
     int64_t t0, t1;
+    const int64_t* rows;    /* NULL: rows t0..t1; else token ids (orc_ffn_rows) */
 } ffn_job;
 
 static void* ffn_worker(void* arg) {
     ffn_job* j = (ffn_job*)arg;
     const int64_t H = j->H, D = j->D;
     float* hidden = (float*)malloc(sizeof(float) * (size_t)D);
-    for (int64_t i = j->t0; i < j->t1; ++i) {
+    for (int64_t ii = j->t0; ii < j->t1; ++ii) {
+        /* rows != NULL: token rows[ii] (orc_ffn_rows), written to out row ii */
+        const int64_t i = j->rows ? j->rows[ii] : ii;
         const float* a = j->A + i * H;
-        float* o = j->out + i * H;
+        float* o = j->out + ii * H;
         for (int64_t x = 0; x < H; ++x) o[x] = 0.0f;
         for (int64_t p = 0; p < j->k; ++p) {
             const int64_t e = j->picks[i * j->k + p];
@@ -259,13 +262,49 @@ void orc_dense_forward(const float* A, const float* Wg, const float* W1, const f
     pthread_t* tids = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)threads);
     for (int t = 0; t < threads; ++t) {
         ffn_job j = {A, W1, B1, W2, B2, H, D, k, act, picks, weights, out,
-                     S * t / threads, S * (t + 1) / threads};
+                     S * t / threads, S * (t + 1) / threads, NULL};
         jobs[t] = j;
     }
     for (int t = 1; t < threads; ++t) pthread_create(&tids[t], NULL, ffn_worker, &jobs[t]);
     ffn_worker(&jobs[0]);
     for (int t = 1; t < threads; ++t) pthread_join(tids[t], NULL);
     free(jobs); free(tids); free(used); free(probs); free(taken); free(tp); free(picks); free(weights);
+}
+
+/* The per-token FFN + combine of oracle.hpp:97-107 for a subset of tokens, given the routing
+ * (picks_e / picks_slot / picks_w as orc_gate returns them; slot -1 = capacity-dropped, which
+ * is exactly the dense oracle's used[e] >= cap test since both count slots in token order).
+ * out row r = output row of token rows[r]; the arithmetic is ffn_worker's, so each row equals
+ * orc_dense_forward's row bit for bit. Lets the tests check sampled rows at full-size shapes. */
+void orc_ffn_rows(const float* A, const float* W1, const float* B1, const float* W2, const float* B2,
+                  int64_t H, int64_t D, int64_t k, int act, const int32_t* picks_e,
+                  const int32_t* picks_slot, const float* picks_w, const int64_t* rows, int64_t n_rows,
+                  float* out, int threads) {
+    int64_t S = 0;
+    for (int64_t r = 0; r < n_rows; ++r) S = rows[r] + 1 > S ? rows[r] + 1 : S;
+    int64_t* picks = (int64_t*)malloc(sizeof(int64_t) * (size_t)(S * k + 1));
+    float* weights = (float*)malloc(sizeof(float) * (size_t)(S * k + 1));
+    for (int64_t r = 0; r < n_rows; ++r) {
+        const int64_t i = rows[r];
+        for (int64_t p = 0; p < k; ++p) {
+            const int kept = picks_slot[i * k + p] >= 0;
+            picks[i * k + p] = kept ? picks_e[i * k + p] : -1;
+            weights[i * k + p] = kept ? picks_w[i * k + p] : 0.0f;
+        }
+    }
+    if (threads < 1) threads = 1;
+    if (threads > n_rows) threads = (int)(n_rows > 0 ? n_rows : 1);
+    ffn_job* jobs = (ffn_job*)malloc(sizeof(ffn_job) * (size_t)threads);
+    pthread_t* tids = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)threads);
+    for (int t = 0; t < threads; ++t) {
+        ffn_job j = {A, W1, B1, W2, B2, H, D, k, act, picks, weights, out,
+                     n_rows * t / threads, n_rows * (t + 1) / threads, rows};
+        jobs[t] = j;
+    }
+    for (int t = 1; t < threads; ++t) pthread_create(&tids[t], NULL, ffn_worker, &jobs[t]);
+    ffn_worker(&jobs[0]);
+    for (int t = 1; t < threads; ++t) pthread_join(tids[t], NULL);
+    free(jobs); free(tids); free(picks); free(weights);
 }
 
 /* oracle.hpp:18-28 */

@@ -67,6 +67,13 @@ void orc_dense_forward(const float* A, const float* Wg, const float* W1, const f
                        const float* W2, const float* B2, int64_t S, int64_t H, int64_t D,
                        int64_t E, int64_t k, int64_t cap, int act, float* out, int threads);
 
+/* oracle.hpp:97-107 for the token ids rows[0..n_rows) only, given orc_gate's picks
+ * (picks_slot -1 = dropped). out: n_rows x H; row r equals orc_dense_forward's row rows[r]. */
+void orc_ffn_rows(const float* A, const float* W1, const float* B1, const float* W2, const float* B2,
+                  int64_t H, int64_t D, int64_t k, int act, const int32_t* picks_e,
+                  const int32_t* picks_slot, const float* picks_w, const int64_t* rows, int64_t n_rows,
+                  float* out, int threads);
+
 /* oracle.hpp:18-28 */
 void orc_naive_matmul(const float* a, const float* b, int64_t m, int64_t k, int64_t n, float* c);
 

@@ -58,6 +58,8 @@ def orc():
         L.orc_gate.argtypes = [vp, vp, i64, i64, i64, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         L.orc_dense_forward.restype = None
         L.orc_dense_forward.argtypes = [vp, vp, vp, vp, vp, vp, i64, i64, i64, i64, i64, i64, C.c_int, vp, C.c_int]
+        L.orc_ffn_rows.restype = None
+        L.orc_ffn_rows.argtypes = [vp, vp, vp, vp, vp, i64, i64, i64, C.c_int, vp, vp, vp, vp, i64, vp, C.c_int]
         L.orc_naive_matmul.restype = None
         L.orc_naive_matmul.argtypes = [vp, vp, i64, i64, i64, vp]
         _orc = L
@@ -79,6 +81,10 @@ def ref():
         L.ref_model_create.restype = vp
         L.ref_model_create.argtypes = [i64, i64, i64, vp, vp, vp, vp, vp]
         L.ref_model_destroy.argtypes = [vp]
+        L.ref_model_synth.restype = vp
+        L.ref_model_synth.argtypes = [vp, C.c_double, C.c_uint64]
+        L.ref_synth_shards.restype = None
+        L.ref_synth_shards.argtypes = [vp, C.c_double, C.c_uint64, vp]
         L.ref_forward.restype = i32
         L.ref_forward.argtypes = [vp, C.c_double, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         L.ref_dense_forward.restype = i32
@@ -132,6 +138,20 @@ def dense_forward(a, model, cfg, cap: Optional[int] = None, threads: int = 1):
     return out
 
 
+def ffn_rows(a, model, cfg, routing, rows, threads: int = 1):
+    """orc_ffn_rows: output rows of the given token ids, from orc_gate routing (dict from gate())."""
+    a = np.ascontiguousarray(a, np.float32)
+    rows = np.ascontiguousarray(rows, np.int64)
+    out = np.empty((rows.size, a.shape[1]), np.float32)
+    pe = np.ascontiguousarray(routing["picks_expert"], np.int32)
+    ps = np.ascontiguousarray(routing["picks_slot"], np.int32)
+    pw = np.ascontiguousarray(routing["picks_weight"], np.float32)
+    orc().orc_ffn_rows(_p(a), _p(model.w1), _p(model.b1), _p(model.w2), _p(model.b2), a.shape[1], cfg.ffn_dim,
+                       cfg.topk, int(cfg.activation), _p(pe), _p(ps), _p(pw), _p(rows), rows.size, _p(out),
+                       threads)
+    return out
+
+
 def expf_libm(x):
     x = np.ascontiguousarray(x, np.float32)
     y = np.empty_like(x)
@@ -141,16 +161,27 @@ def expf_libm(x):
 
 # ------------------------------------------------------------------ the reference itself
 class RefModel:
-    def __init__(self, model, cfg):
+    def __init__(self, model, cfg, seed: Optional[int] = None):
+        """model=None: the reference harness's seeded model built inside the shim (harness.hpp:76-97)."""
         self.cfg = cfg
-        self._h = ref().ref_model_create(cfg.embed_dim, cfg.ffn_dim, cfg.experts_total, _p(model.wg),
-                                         _p(model.w1), _p(model.b1), _p(model.w2), _p(model.b2))
+        if model is None:
+            self._h = ref().ref_model_synth(_p(_cfgv(cfg)), cfg.capacity_factor, cfg.seed if seed is None else seed)
+        else:
+            self._h = ref().ref_model_create(cfg.embed_dim, cfg.ffn_dim, cfg.experts_total, _p(model.wg),
+                                             _p(model.w1), _p(model.b1), _p(model.w2), _p(model.b2))
 
     def __del__(self):
         try:
             ref().ref_model_destroy(self._h)
         except Exception:
             pass
+
+
+def ref_synth_shards(cfg, seed: Optional[int] = None):
+    """harness.hpp:99-109 shards (P x S x H) from the shim."""
+    out = np.empty((cfg.devices, cfg.tokens_per_device, cfg.embed_dim), np.float32)
+    ref().ref_synth_shards(_p(_cfgv(cfg)), cfg.capacity_factor, cfg.seed if seed is None else seed, _p(out))
+    return [out[d] for d in range(cfg.devices)]
 
 
 def ref_forward(cfg, shards, refmodel: RefModel, processors: int = 4, sequential: bool = False):

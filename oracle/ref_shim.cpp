@@ -8,8 +8,10 @@
 //   moefabric::gate_forward                (gate.hpp:108)
 // so the repo's oracle restatement and the CUDA operator can be checked against
 // the reference itself, and bench.py can time the reference's CPU path.
+#include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <random>
 #include <exception>
 #include <string>
 #include <vector>
@@ -74,6 +76,46 @@ void* ref_model_create(int64_t H, int64_t D, int64_t E, const float* wg, const f
 }
 
 void ref_model_destroy(void* m) { delete static_cast<ModelWeights*>(m); }
+
+// The reference harness's seeded model (harness.hpp:76-97, restated because harness.hpp itself
+// needs the absent vendor/ JSON library): Wg, W1 ~ N(0,1)/sqrt(H), W2 ~ N(0,1)/sqrt(D),
+// b ~ 0.1 N(0,1), one mt19937_64 stream in this draw order. Lets bench.py's reference arm build its
+// inputs without loading the product library.
+void* ref_model_synth(const int64_t* cfgv, double cf, uint64_t seed) {
+    const MoeConfig cfg = make_cfg(cfgv, cf);
+    std::mt19937_64 rng(seed);
+    std::normal_distribution<float> dist(0.0f, 1.0f);
+    const float s1 = 1.0f / std::sqrt(static_cast<float>(cfg.embed_dim));
+    const float s2 = 1.0f / std::sqrt(static_cast<float>(cfg.ffn_dim));
+    auto* m = new ModelWeights();
+    m->gate.wg = TokenMatrix(cfg.embed_dim, cfg.experts_total);
+    for (auto& v : m->gate.wg.data) v = dist(rng) * s1;
+    m->experts.resize(static_cast<size_t>(cfg.experts_total));
+    for (auto& ep : m->experts) {
+        ep.w1 = TokenMatrix(cfg.embed_dim, cfg.ffn_dim);
+        for (auto& v : ep.w1.data) v = dist(rng) * s1;
+        ep.b1.assign(static_cast<size_t>(cfg.ffn_dim), 0.0f);
+        for (auto& v : ep.b1) v = 0.1f * dist(rng);
+        ep.w2 = TokenMatrix(cfg.ffn_dim, cfg.embed_dim);
+        for (auto& v : ep.w2.data) v = dist(rng) * s2;
+        ep.b2.assign(static_cast<size_t>(cfg.embed_dim), 0.0f);
+        for (auto& v : ep.b2) v = 0.1f * dist(rng);
+    }
+    return m;
+}
+
+// harness.hpp:99-109: device d's tokens from mt19937_64(seed ^ 0xD1B54A32D192ED03 * (d + 1)).
+// out: P x S x H.
+void ref_synth_shards(const int64_t* cfgv, double cf, uint64_t seed, float* out) {
+    const MoeConfig cfg = make_cfg(cfgv, cf);
+    const int64_t n = cfg.tokens_per_device * cfg.embed_dim;
+    for (int64_t d = 0; d < cfg.devices; ++d) {
+        std::mt19937_64 rng(seed ^ (0xD1B54A32D192ED03ull * (static_cast<uint64_t>(d) + 1)));
+        std::normal_distribution<float> dist(0.0f, 1.0f);
+        float* a = out + d * n;
+        for (int64_t i = 0; i < n; ++i) a[i] = dist(rng);
+    }
+}
 
 // forward(): cfgv = {S, H, D, E, P, k, bM, bN, act}. shards/out: P x S x H.
 // Routing outputs per device: tbl_tok/tbl_w P x E x cap, slot_counts P x E,

@@ -1204,12 +1204,16 @@ struct GemmCfg {
     static constexpr int KSTEP = PREC == kFP32 ? 8 : 16;       // K per tcgen05.mma
     static constexpr int KSTEPS = BK / KSTEP;                   // 8
     static constexpr int STEPS_PER_ATOM = ATOM_K / KSTEP;       // 4
-    static constexpr int A_COLS = PREC == kFP32 ? 2 * BK : BK / 2;   // TMEM columns per weight stage
+    // TMEM weight operand. bf16: one slot per stage (BK/2 columns), STAGES deep, after the two
+    // accumulators. FP32: a 2-deep ring of half-stages (one 128-byte atom = 32 K: 32 hi + 32 lo
+    // columns) after the two accumulators and the tile's correction accumulator (kTmemCorr).
+    static constexpr int A_COLS = PREC == kFP32 ? 2 * ATOM_K : BK / 2;
+    static constexpr int A_SLOTS = PREC == kFP32 ? 2 : STAGES;
     static constexpr uint32_t IDESC = umma_idesc(PREC == kFP32 ? 2u : 1u, kBF, kNT);
     static constexpr int W_OFF = STAGE_BYTES * STAGES;
     static constexpr int RING_BYTES = W_OFF + W_BYTES * WSTAGES;
-    static constexpr uint32_t TMEM_A0 = kAccStages * kNT;      // first weight-stage column
-    static_assert(TMEM_A0 + STAGES * A_COLS <= 512, "TMEM budget");
+    static constexpr uint32_t TMEM_A0 = PREC == kFP32 ? kTmemCorr + kNT : kAccStages * kNT;
+    static_assert(TMEM_A0 + A_SLOTS * A_COLS <= 512, "TMEM budget");
 };
 
 // dynamic smem: [max(gate scratch, FFN rings)] [GemmCtrl]
@@ -1222,7 +1226,9 @@ struct SmemPlan {
 };
 
 struct GemmCtrl {
-    uint64_t ready[8], done[8];                      // token smem ring + weight TMEM ring (same stages)
+    uint64_t ready[8], done[8];                      // token smem ring (+ bf16: the weight TMEM ring, same stages)
+    uint64_t afull[2], aempty[2];                    // FP32: weight TMEM half-stage ring (converters <-> MMA)
+    uint64_t cempty;                                 // FP32: correction accumulator folded (epilogue -> MMA)
     uint64_t wfull[8], wempty[8];                    // weight smem ring (producer -> converters)
     uint64_t tfull[kAccStages], tempty[kAccStages];  // accumulators
     uint64_t qfull[kTaskRing], qempty[kTaskRing];    // task ring
@@ -1234,7 +1240,10 @@ struct GemmCtrl {
 };
 static_assert(sizeof(GemmCtrl) <= 1024, "GemmCtrl fits the control area");
 constexpr int kTaskConsumers = 1 + 4 + 1;   // MMA warp, 4 converter warps, epilogue
-constexpr int kReadyCount = 1 + 4;          // producer (expect_tx) + 4 converter warps
+template <int PREC>
+struct ReadyCount {   // bf16: producer (expect_tx) + 4 converter warps; FP32: producer (tokens only)
+    static constexpr int N = PREC == kFP32 ? 1 : 1 + 4;
+};
 
 __device__ __forceinline__ void decode_task(const LaunchParams& P, uint32_t t, uint32_t n_g0, Task& tk) {
     const bool g1 = t >= n_g0;
@@ -1429,14 +1438,14 @@ __device__ void gemm_wconvert(const LaunchParams& P, uint8_t* ring, GemmCtrl& G,
             if (++wst == Cfg::WSTAGES) { wst = 0; wphase ^= 1u; }
 
             const long long c2 = clk();
-            if (!FD_TIMED_WAIT(w_a, mbar_wait(&G.done[ast], aphase ^ 1u, P.abort_flag))) return;
-            const long long c3 = clk();
-            tc_fence_after();
-            const uint32_t col = tmem + lane_addr + Cfg::TMEM_A0 + ast * Cfg::A_COLS;
-            if (P.debug & kDbgNoConvert) {
-            } else if (PREC == kFP32) {
+            if constexpr (PREC == kFP32) {
+                // one TMEM half-stage per 128-byte atom (32 K values: hi columns [0, 32), lo [32, 64)),
+                // each released to the MMA warp on its own so the ring runs half a stage ahead
 #pragma unroll
-                for (int at = 0; at < Cfg::NATOM; ++at)
+                for (int at = 0; at < Cfg::NATOM; ++at) {
+                    if (!FD_TIMED_WAIT(w_a, mbar_wait(&G.aempty[ast], aphase ^ 1u, P.abort_flag))) return;
+                    tc_fence_after();
+                    const uint32_t col = tmem + lane_addr + Cfg::TMEM_A0 + ast * Cfg::A_COLS;
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {   // 16 K values per half atom
                         uint32_t hi[16], lo[16];
@@ -1451,10 +1460,22 @@ __device__ void gemm_wconvert(const LaunchParams& P, uint8_t* ring, GemmCtrl& G,
                                 lo[i * 4 + u] = __float_as_uint(__fsub_rn(vv[u], hv));
                             }
                         }
-                        const int k0 = at * Cfg::ATOM_K + h * 16;
-                        tmem_st16(col + k0, hi);             // hi: columns [0, BK)
-                        tmem_st16(col + Cfg::BK + k0, lo);   // lo: columns [BK, 2 BK)
+                        tmem_st16(col + h * 16, hi);                  // hi: columns [0, 32)
+                        tmem_st16(col + Cfg::ATOM_K + h * 16, lo);    // lo: columns [32, 64)
                     }
+                    tmem_wait_st();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&G.afull[ast]);
+                    if (++ast == Cfg::A_SLOTS) { ast = 0; aphase ^= 1u; }
+                }
+                continue;
+            }
+            if (!FD_TIMED_WAIT(w_a, mbar_wait(&G.done[ast], aphase ^ 1u, P.abort_flag))) return;
+            const long long c3 = clk();
+            tc_fence_after();
+            const uint32_t col = tmem + lane_addr + Cfg::TMEM_A0 + ast * Cfg::A_COLS;
+            if (P.debug & kDbgNoConvert) {
             } else {
 #pragma unroll
                 for (int at = 0; at < Cfg::NATOM; ++at)
@@ -1523,6 +1544,76 @@ __device__ __forceinline__ void issue_stage(uint32_t d_tmem, uint32_t abase, uin
     }
 }
 
+// FP32 (3xTF32) MMAs of one half-stage (one 128-byte token atom = 4 k-steps). The tcgen05 FP32
+// accumulator rounds toward zero once per MMA (measured: tools/dev/acc_probe.py, profiles/r02_numerics.md),
+// so the error of one accumulator grows with the number of MMAs folded into it. The w_hi*x_hi products
+// go to the tile's main accumulator (K/8 MMAs), the two correction products (2^-11 smaller) to a
+// separate correction accumulator that the epilogue adds in round-to-nearest FP32: a third of the
+// main accumulator's truncations, and the corrections' own truncations are 2^-11 smaller.
+// CORR_FIRST: corrections then main (back-to-back MMAs never read the same TMEM A columns either way).
+template <bool MAIN, bool CORR>
+__device__ __forceinline__ void issue_half_fp32(uint32_t d_main, uint32_t d_corr, uint32_t a_half, uint64_t bdesc,
+                                                uint32_t main_acc, uint32_t corr_acc) {
+    using Cfg = GemmCfg<kFP32>;
+    if (CORR) {
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)   // w_lo * x_hi
+            mma_tf32_ts(d_corr, a_half + Cfg::ATOM_K + ks * Cfg::KSTEP, bdesc + ((ks * 32) >> 4),
+                        Cfg::IDESC, ks == 0 ? corr_acc : 1u);
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)   // w_hi * x_lo
+            mma_tf32_ts(d_corr, a_half + ks * Cfg::KSTEP,
+                        bdesc + ((Cfg::PLANE_BYTES + ks * 32) >> 4), Cfg::IDESC, 1u);
+    }
+    if (MAIN) {
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)   // w_hi * x_hi
+            mma_tf32_ts(d_main, a_half + ks * Cfg::KSTEP, bdesc + ((ks * 32) >> 4), Cfg::IDESC,
+                        ks == 0 ? main_acc : 1u);
+    }
+}
+
+struct MmaFp32State {
+    int stage = 0, ah = 0;
+    uint32_t phase = 0, ahph = 0, cph = 0;
+};
+
+// One FP32 tile on the MMA warp (one lane): token stages of 2 atoms (ready/done), weight half-stages
+// (afull/aempty), main accumulator d_main, correction accumulator kTmemCorr (freed by the epilogue's
+// fold of the previous tile: cempty). The tile's first half-stage issues its main MMAs before waiting
+// for the fold, so the fold overlaps them.
+__device__ __forceinline__ bool mma_tile_fp32(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, uint32_t tmem,
+                                              uint32_t d_main, int nk, MmaFp32State& st, long long& w_x) {
+    using Cfg = GemmCfg<kFP32>;
+    const uint32_t d_corr = tmem + kTmemCorr;
+    for (int kb = 0; kb < nk; ++kb) {
+        if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.ready[st.stage], st.phase, P.abort_flag))) return false;
+        tc_fence_after();
+        const uint64_t bdesc = umma_desc_kmajor(smem_u32(ring + st.stage * Cfg::STAGE_BYTES), 128);
+#pragma unroll
+        for (int at = 0; at < Cfg::NATOM; ++at) {
+            if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.afull[st.ah], st.ahph, P.abort_flag))) return false;
+            tc_fence_after();
+            const uint32_t a_half = tmem + Cfg::TMEM_A0 + st.ah * Cfg::A_COLS;
+            const uint64_t bd = bdesc + ((at * Cfg::ATOM_BYTES) >> 4);
+            if (kb == 0 && at == 0) {
+                issue_half_fp32<true, false>(d_main, d_corr, a_half, bd, 0u, 0u);
+                if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.cempty, st.cph ^ 1u, P.abort_flag))) return false;
+                st.cph ^= 1u;
+                tc_fence_after();
+                issue_half_fp32<false, true>(d_main, d_corr, a_half, bd, 0u, 0u);
+            } else {
+                issue_half_fp32<true, true>(d_main, d_corr, a_half, bd, 1u, 1u);
+            }
+            mma_commit(&G.aempty[st.ah]);
+            if (++st.ah == Cfg::A_SLOTS) { st.ah = 0; st.ahph ^= 1u; }
+        }
+        mma_commit(&G.done[st.stage]);
+        if (++st.stage == Cfg::STAGES) { st.stage = 0; st.phase ^= 1u; }
+    }
+    return true;
+}
+
 template <int PREC>
 __device__ void gemm_mma(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, unsigned long long* trace,
                          unsigned long long* chunklog) {
@@ -1541,6 +1632,7 @@ __device__ void gemm_mma(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, unsi
     const uint32_t abase_s[2] = {tmem + Cfg::TMEM_A0, tmem + Cfg::TMEM_A0 + Cfg::A_COLS};
     const uint64_t bdesc_s[2] = {umma_desc_kmajor(smem_u32(ring), 128),
                                  umma_desc_kmajor(smem_u32(ring + Cfg::STAGE_BYTES), 128)};
+    MmaFp32State st32;
     while (true) {
         if (!FD_TIMED_WAIT(w_task, mbar_wait(&G.qfull[q], qphase, P.abort_flag))) return;
         const int type = G.ring[q].type;
@@ -1555,6 +1647,12 @@ __device__ void gemm_mma(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, unsi
         const int nk = ((type == 0 ? P.H : P.D) + Cfg::BK - 1) / Cfg::BK;
         if (!FD_TIMED_WAIT(w_acc, mbar_wait(&G.tempty[acc], accphase ^ 1u, P.abort_flag))) return;
         const uint32_t d_tmem = tmem + (uint32_t)(acc * kNT);
+        if constexpr (PREC == kFP32) {
+            if (!mma_tile_fp32(P, ring, G, tmem, d_tmem, nk, st32, w_x)) return;
+            mma_commit(&G.tfull[acc]);   // main + correction accumulators ready for the epilogue
+            if (++acc == kAccStages) { acc = 0; accphase ^= 1u; }
+            continue;
+        }
         long long t_rdy = chunklog ? clk() : 0;
         if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.ready[stage], phase, P.abort_flag))) return;
         tc_fence_after();
@@ -1665,6 +1763,23 @@ __device__ void gemm_signal(const LaunchParams& P, const RankCtx& R, GemmCtrl& G
     }
 }
 
+// FP32: add the tile's correction accumulator into its main accumulator in round-to-nearest FP32
+// (this warp's 32 TMEM lanes, 128 token columns), leaving the correction columns free.
+__device__ __forceinline__ void fold_corr(uint32_t t_main, uint32_t t_corr) {
+#pragma unroll 1
+    for (int ch = 0; ch < kNT / 32; ++ch) {
+        uint32_t m[32], c[32];
+        tmem_ld32(t_main + ch * 32, m);
+        tmem_ld32(t_corr + ch * 32, c);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) m[i] = __float_as_uint(__fadd_rn(__uint_as_float(m[i]), __uint_as_float(c[i])));
+        tmem_st32(t_main + ch * 32, m);
+    }
+    tmem_wait_st();
+    tc_fence_before();
+}
+
 // GEMM0 epilogue of one 32-token chunk: +b1, activation, store C1 (tf32 hi/lo planes or bf16).
 // Row i of the chunk lives at +i*D; bit i of vmask = row holds a landed token (warp-uniform).
 template <int PREC, int ACT>
@@ -1734,6 +1849,12 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
         }
         if (!FD_TIMED_WAIT(w_acc, mbar_wait(&G.tfull[acc], accphase, P.abort_flag))) return;
         tc_fence_after();
+        if constexpr (PREC == kFP32) {   // main += corrections (RN), then the MMA warp may reuse kTmemCorr
+            const uint32_t lanes = (uint32_t)(wq * 32) << 16;
+            fold_corr(tmem + lanes + (uint32_t)(acc * kNT), tmem + lanes + kTmemCorr);
+            __syncwarp();
+            if ((et & 31) == 0) mbar_arrive(&G.cempty);
+        }
         if (FUSED && type == 1 && !zero_seen) {
             for (int r = 0; r < P.nranks; ++r)
                 if (!wait_counter(P, R, P.ranks[r].zero_ctr, P.zero_target, 310)) return;
@@ -2020,8 +2141,10 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
 
     // phase 3: expert FFN tiles
     if (tid == 0) {
-        for (int i = 0; i < Cfg::STAGES; ++i) { mbar_init(&G.ready[i], kReadyCount); mbar_init(&G.done[i], 1); }
+        for (int i = 0; i < Cfg::STAGES; ++i) { mbar_init(&G.ready[i], ReadyCount<PREC>::N); mbar_init(&G.done[i], 1); }
         for (int i = 0; i < Cfg::WSTAGES; ++i) { mbar_init(&G.wfull[i], 1); mbar_init(&G.wempty[i], 4); }
+        for (int i = 0; i < 2; ++i) { mbar_init(&G.afull[i], 4); mbar_init(&G.aempty[i], 1); }
+        mbar_init(&G.cempty, 4);
         for (int i = 0; i < kAccStages; ++i) { mbar_init(&G.tfull[i], 1); mbar_init(&G.tempty[i], 1); }
         for (int i = 0; i < kTaskRing; ++i) { mbar_init(&G.qfull[i], 1); mbar_init(&G.qempty[i], kTaskConsumers); }
         for (int i = 0; i < kTaskRing; ++i) { mbar_init(&G.sfull[i], 1); mbar_init(&G.sempty[i], 1); }
@@ -2123,8 +2246,10 @@ __global__ void __launch_bounds__(kThreads, 1) debug_gemm_kernel(const __grid_co
     const int tid = threadIdx.x, warp = tid >> 5;
     if (warp == kWarpTmem) { tmem_alloc(&G.tmem_base, 512); tmem_relinquish(); }
     if (tid == 0) {
-        for (int i = 0; i < Cfg::STAGES; ++i) { mbar_init(&G.ready[i], kReadyCount); mbar_init(&G.done[i], 1); }
+        for (int i = 0; i < Cfg::STAGES; ++i) { mbar_init(&G.ready[i], ReadyCount<PREC>::N); mbar_init(&G.done[i], 1); }
         for (int i = 0; i < Cfg::WSTAGES; ++i) { mbar_init(&G.wfull[i], 1); mbar_init(&G.wempty[i], 4); }
+        for (int i = 0; i < 2; ++i) { mbar_init(&G.afull[i], 4); mbar_init(&G.aempty[i], 1); }
+        mbar_init(&G.cempty, 4);
         mbar_init(&G.tfull[0], 1);
         for (int i = 0; i < kTaskRing; ++i) { mbar_init(&G.qfull[i], 1); mbar_init(&G.qempty[i], kTaskConsumers); }
         G.ring[0].type = 0;
@@ -2157,15 +2282,23 @@ __global__ void __launch_bounds__(kThreads, 1) debug_gemm_kernel(const __grid_co
             if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
         }
     } else if (tid == kWarpMma * 32) {
-        int stage = 0; uint32_t phase = 0;
-        for (int kb = 0; kb < nk; ++kb) {
-            mbar_wait(&G.ready[stage], phase, abort_flag);
-            tc_fence_after();
-            issue_stage<PREC, 0, StageMmas<PREC>::N>(tmem, tmem + Cfg::TMEM_A0 + stage * Cfg::A_COLS,
-                                                     umma_desc_kmajor(smem_u32(smem + stage * Cfg::STAGE_BYTES), 128),
-                                                     kb == 0);
-            mma_commit(&G.done[stage]);
-            if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
+        if constexpr (PREC == kFP32) {
+            LaunchParams P{};
+            P.abort_flag = abort_flag;
+            MmaFp32State st;
+            long long w = 0;
+            mma_tile_fp32(P, smem, G, tmem, tmem, nk, st, w);
+        } else {
+            int stage = 0; uint32_t phase = 0;
+            for (int kb = 0; kb < nk; ++kb) {
+                mbar_wait(&G.ready[stage], phase, abort_flag);
+                tc_fence_after();
+                issue_stage<PREC, 0, StageMmas<PREC>::N>(tmem, tmem + Cfg::TMEM_A0 + stage * Cfg::A_COLS,
+                                                         umma_desc_kmajor(smem_u32(smem + stage * Cfg::STAGE_BYTES), 128),
+                                                         kb == 0);
+                mma_commit(&G.done[stage]);
+                if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
+            }
         }
         mma_commit(&G.tfull[0]);
     } else if (warp >= kWarpConv0 && warp < kWarpConv0 + 4) {
@@ -2176,6 +2309,7 @@ __global__ void __launch_bounds__(kThreads, 1) debug_gemm_kernel(const __grid_co
         const int et = tid - kWarpEpi0 * 32, wq = et >> 5;
         mbar_wait(&G.tfull[0], 0, abort_flag);
         tc_fence_after();
+        if (PREC == kFP32) fold_corr(tmem + ((uint32_t)(wq * 32) << 16), tmem + ((uint32_t)(wq * 32) << 16) + kTmemCorr);
         for (int ch = 0; ch < kNT / 32; ++ch) {
             uint32_t r[32];
             tmem_ld32(tmem + ((uint32_t)(wq * 32) << 16) + ch * 32, r);

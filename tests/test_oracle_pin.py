@@ -93,3 +93,36 @@ def test_oracle_matches_golden_fixture(path):
         g = po.gate(shards[d], model.wg, k, cap)
         assert np.array_equal(g["table_token"][:, :cap], z["table_token"][d])
         assert np.array_equal(g["g_phi"].view(np.uint32), z["g_phi"][d].view(np.uint32))
+
+
+@pytest.mark.parametrize("S,H,D,E,P,k,cf,act", CONFIGS)
+def test_ffn_rows_equals_dense_rows(S, H, D, E, P, k, cf, act):
+    """orc_ffn_rows (the sampled-row checker of tests/test_gpu_baseline.py) reproduces
+    orc_dense_forward's rows bit for bit from orc_gate's routing."""
+    cfg = _cfg(S, H, D, E, 1, k, cf, act)
+    model = fd.make_model(cfg)
+    shard = fd.make_shards(cfg)[0]
+    routing = po.gate(shard, model.wg, k, fd.expert_capacity(cfg))
+    full = po.dense_forward(shard, model, cfg, threads=3)
+    rows = np.array(sorted(set([0, S - 1, S // 2, 1, S // 3])), np.int64)
+    got = po.ffn_rows(shard, model, cfg, routing, rows, threads=2)
+    assert np.array_equal(got.view(np.uint32), full[rows].view(np.uint32))
+
+
+@needs_ref
+@pytest.mark.parametrize("S,H,D,E,P,k,cf,act", CONFIGS[:2])
+def test_reference_arm_inputs_match_product_generator(S, H, D, E, P, k, cf, act):
+    """bench.py --impl reference builds its model and shards inside oracle/_ref (harness.hpp:76-109,
+    no product library); they are byte-identical to the product's fdmoe_synth_* inputs, so both arms
+    run the same layer on the same bytes."""
+    cfg = _cfg(S, H, D, E, P, k, cf, act, seed=5)
+    model = fd.make_model(cfg)
+    shards = fd.make_shards(cfg)
+    rshards = po.ref_synth_shards(cfg)
+    for a, b in zip(shards, rshards):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    rm_synth = po.RefModel(None, cfg)
+    rm_copy = po.RefModel(model, cfg)
+    o1 = po.ref_dense_forward(cfg, shards[0], rm_synth)
+    o2 = po.ref_dense_forward(cfg, shards[0], rm_copy)
+    assert np.array_equal(o1.view(np.uint32), o2.view(np.uint32))
