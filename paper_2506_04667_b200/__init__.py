@@ -597,13 +597,14 @@ class Operator:
         """Per-CTA phase timestamps of the last launch (ns, relative to the earliest CTA start):
         columns start, gate, barrier, dispatch, ffn, combine, end, ffn_tiles."""
         info = self.info()
-        buf = np.zeros((info["ctas_per_rank"], 28), np.uint64)
+        buf = np.zeros((info["ctas_per_rank"], 32), np.uint64)
         n = C.c_int32()
         _check(lib().fdmoe_read_trace(self._h, local_rank, _ptr(buf), buf.size, C.byref(n)))
         t = buf.astype(np.int64)
         t0 = t[:, 0].min()
         t[:, :7] -= t0
         t[:, 20:27] -= t0
+        t[:, 28] = np.where(t[:, 28] > 0, t[:, 28] - t0, 0)   # tensor-core gate logits done (0: SIMT gate)
         return t
 
     def events(self, local_rank: int = 0) -> np.ndarray:

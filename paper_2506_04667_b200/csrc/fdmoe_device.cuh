@@ -30,7 +30,7 @@ constexpr int kMaxRanks = 64;       // P envelope (peer table size)
 constexpr int kMaxSrcPerTile = 8;   // packet_rows >= 16 -> <= 8 packets per 128-row tile
 constexpr int kCombineTok = 16;     // tokens per combine task (== kGateTok)
 constexpr int kMaxLocalRanks = 8;   // ranks per launch (virtual ranks on one GPU)
-constexpr int kTracePts = 28;
+constexpr int kTracePts = 32;
 constexpr int kGroupBarriers = 2;   // sequential mode: after dispatch, after the expert FFN
 constexpr int kChunkLog = 512;       // start, gate, barrier, dispatch, gemm, combine, end, tiles,
                                     // then FFN pipeline wait cycles (see kWait*)
@@ -38,7 +38,8 @@ enum WaitSlot : int {
     kWaitMmaX = 8, kWaitMmaA, kWaitMmaAcc, kWaitConvW, kWaitConvA, kWaitProdW, kWaitProdX, kWaitEpiAcc,
     kWaitMmaTask, kProdFetch, kEpiBusy, kMmaTiles,
     kTrPrefix = 20, kTrSlots, kTrSlotBarrier, kTrPush,   // dispatch sub-phases (%globaltimer)
-    kTrGateLogits = 24, kTrGatePairs, kTrGateFull, kTrGateNFull   // gate sub-phases (last sub-tile), full tokens
+    kTrGateLogits = 24, kTrGatePairs, kTrGateFull, kTrGateNFull,  // gate sub-phases (last sub-tile), full tokens
+    kTrGateTc = 28                                                // tensor-core gate logits done
 };
 
 enum Prec : int { kFP32 = 0, kBF16 = 1 };
@@ -69,6 +70,7 @@ struct alignas(64) RankCtx {
     CUtensorMap tm_c1[2];      // [hi|lo]          rows = E_local*RP, cols = D
     CUtensorMap tm_w1;         // W1^T [E_local*D (+pad)][H], FP32 (split on chip) or bf16, box 128 rows
     CUtensorMap tm_w2;         // W2^T [E_local*H (+pad)][D]
+    CUtensorMap tm_wg[2];      // tensor-core gate: Wg^T tf32 [hi|lo] planes [gate_nblk * gate_n][H], box gate_n rows
 
     uint8_t* peer_heap[kMaxRanks];   // heap base of rank q as mapped here (q == rank: own)
     HeapLayout hl;
@@ -80,6 +82,8 @@ struct alignas(64) RankCtx {
     const float* wg;           // [H][E_total]
     const float* wg_norm;      // [E_total] |Wg[:, e]|_2 rounded up (certified gate)
     const float* wgT;          // [E_total][H] Wg transposed (certified gate's exact pair pass)
+    double* gate_na;           // [S] tensor-core gate: sum of squares of each token row (converter warps)
+    float* gate_sab;           // [S] tensor-core gate: sum over 64-K chunk ends of max_e |prefix logit|
     float* g_phi;              // [S][E_total]
     int32_t* pick_e;           // [S][k]
     int32_t* pick_slot;        // [S][k]  (-1 = capacity-dropped)
@@ -108,6 +112,7 @@ struct alignas(64) RankCtx {
 };
 
 struct LaunchParams {
+    CUtensorMap tm_in[kMaxLocalRanks];   // tensor-core gate: each local rank's input shard [S][H] FP32, box 128 rows
     RankCtx* ranks;            // device array, one per rank in this launch
     const float* in[kMaxLocalRanks];
     float* out[kMaxLocalRanks];
@@ -130,6 +135,10 @@ struct LaunchParams {
     int exact_gate;            // 1: reference-exact logits for every token (bit-exact G_phi, weights)
     float gate_u;              // certified gate: u' = 2^-24 * 1.001
     float gate_k1;             // certified gate: 66 + 2 H gamma_{H+1}
+    int gate_tc;               // 1: gate logits on the tensor cores (3xTF32), certified with gate_k1_tc
+    int gate_n;                // tensor-core gate: MMA N (experts per block, multiple of 16, <= 128)
+    int gate_nblk;             // tensor-core gate: expert blocks of gate_n
+    float gate_k1_tc;          // tensor-core gate: |z~ - z_ref| <= gate_u * gate_k1_tc * |a| |w_e|
 };
 enum DebugBits : int {
     kDbgNoConvert = 1,    // converter warps skip the split + tcgen05.st (MMA reads stale TMEM)
@@ -378,6 +387,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
           "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
           "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
           "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr)
+        : "memory");
+}
+// 32 lanes x 16 consecutive 32-bit columns.
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
         : "r"(taddr)
         : "memory");
 }

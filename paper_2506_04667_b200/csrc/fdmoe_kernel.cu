@@ -581,8 +581,10 @@ __device__ int route_certified(const LaunchParams& P, const RankCtx& R, float* r
     constexpr int J = kMaxExperts / 32;
     const int E = P.E, K = P.k, lane = threadIdx.x & 31;
     const float na = __double2float_ru(sqrt(g.sNa[t] * (1.0 + 1e-5)));
+    // SIMT logits: chunk-end partial sums (sSab) + product / chain-distance terms; tensor-core logits:
+    // sSab = 0 and the whole bound rides on |a| |w_e| (gate_k1_tc, set by the host)
     const float c_s = P.gate_u * 64.0f * g.sSab[t];
-    const float c_w = P.gate_u * P.gate_k1 * na;
+    const float c_w = P.gate_u * (P.gate_tc ? P.gate_k1_tc : P.gate_k1) * na;
     float z[J], bt[J];
     bool bad = false;
 #pragma unroll
@@ -888,7 +890,17 @@ __device__ void gate_phase(const LaunchParams& P, const RankCtx& R, const float*
         for (int t = tid; t < ts; t += kThreads) { g.sSab[t] = 0.0f; g.sTNC[t] = 0; }
         if (tid == 0) { s_np = 0; s_nfull = 0; }
         __syncthreads();
-        if (small) gate_logits<true, 1, 4>(P, R, A, tokA + s0, nullptr, ts, g);
+        if (P.gate_tc) {   // tensor-core logits (phase 1a) and row norms from global
+            for (int i = tid; i < ts * Ep; i += kThreads) {
+                const int t = i / Ep, e = i - t * Ep;
+                g.sL[i] = e < E ? R.g_phi[(size_t)(tokA + s0 + t) * E + e] : 0.0f;
+            }
+            for (int t = tid; t < ts; t += kThreads) {
+                g.sNa[t] = R.gate_na[tokA + s0 + t];
+                g.sSab[t] = R.gate_sab[tokA + s0 + t];
+            }
+            __syncthreads();
+        } else if (small) gate_logits<true, 1, 4>(P, R, A, tokA + s0, nullptr, ts, g);
         else gate_logits<true, kGateTT, kGateTE>(P, R, A, tokA + s0, nullptr, ts, g);
         for (int t = warp; t < ts; t += kWarps) {
             const int r = route_certified(P, R, g.sL + t * Ep, tokA + s0 + t, t, g, &s_np);
@@ -1175,13 +1187,18 @@ __device__ void push_phase(const LaunchParams& P, const RankCtx& R, const float*
 // element. B operand (tokens, already hi/lo-split by the sender at dispatch) is TMA-staged in a
 // SWIZZLE_128B smem ring. 3xTF32: lo*hi + hi*lo + hi*hi per k-step (product-major), FP32
 // accumulation in double-buffered TMEM accumulators. (runtime.hpp:652-699, tiled_blas.hpp:80-96)
+constexpr int kGateTask = 2;
 struct Task {
-    int type;   // 0 = GEMM0, 1 = GEMM1, -1 = end
+    int type;   // 0 = GEMM0, 1 = GEMM1, 2 = gate logits tile (kGateTask), -1 = end
+                // gate tile: m = first token, nb = expert block, cnt[0] = valid token rows
     int le, nb, m;
     int nsrc, src0;
     int cnt[kMaxSrcPerTile];   // valid rows per packet in the tile
     uint64_t t0;               // event log: dependencies resolved, operand streaming starts
 };
+
+// K extent of a task: GEMM0 and gate tiles contract over H, GEMM1 over D.
+__device__ __forceinline__ int task_k(const LaunchParams& P, int type) { return type == 1 ? P.D : P.H; }
 
 // Stage = BK elements of K = NATOM SWIZZLE_128B atoms (128-byte rows). One wait + one commit per
 // stage: ready[s] completes when the token TMA bytes landed AND the 4 converter warps stored the
@@ -1217,12 +1234,15 @@ struct GemmCfg {
 };
 
 // dynamic smem: [max(gate scratch, FFN rings)] [GemmCtrl]
+// (the tensor-core gate runs the FP32 pipeline in either precision's kernel, so the region covers both rings;
+//  the FFN and the gate each get their own control block)
+constexpr int cmax(int a, int b) { return a > b ? a : b; }
 template <int PREC>
 struct SmemPlan {
-    static constexpr int REGION = ((kGateSmemBytes > GemmCfg<PREC>::RING_BYTES ? kGateSmemBytes
-                                                                                : GemmCfg<PREC>::RING_BYTES) +
-                                   1023) / 1024 * 1024;
-    static constexpr int TOTAL = REGION + 1024 /* ctrl */ + 1024 /* alignment slack */;
+    static constexpr int REGION =
+        (cmax(kGateSmemBytes, cmax(GemmCfg<kFP32>::RING_BYTES, GemmCfg<kBF16>::RING_BYTES)) + 1023) / 1024 * 1024;
+    static constexpr int CTRL_GATE = REGION + 1024;
+    static constexpr int TOTAL = REGION + 2048 /* ctrl: FFN, gate */ + 1024 /* alignment slack */;
 };
 
 struct GemmCtrl {
@@ -1361,7 +1381,7 @@ __device__ void gemm_producer(const LaunchParams& P, const RankCtx& R, uint8_t* 
         else { tb[0] = &R.tm_c1[0]; tb[1] = &R.tm_c1[1]; tw = &R.tm_w2; yw = tk.le * P.H; }
         yw += tk.nb * kBF;
         const int y = tk.le * P.RP + tk.m * kBM;
-        const int nk = ((tk.type == 0 ? P.H : P.D) + Cfg::BK - 1) / Cfg::BK;
+        const int nk = (task_k(P, tk.type) + Cfg::BK - 1) / Cfg::BK;
         for (int kb = 0; kb < nk; ++kb) {
             // weight tile first: the converter warps need it one step before the MMA does
             if (!FD_TIMED_WAIT(w_w, mbar_wait(&G.wempty[wstage], wphase ^ 1u, P.abort_flag))) return;
@@ -1396,9 +1416,11 @@ __device__ void gemm_producer(const LaunchParams& P, const RankCtx& R, uint8_t* 
 // tcgen05.st into the TMEM weight ring. Thread (warp 4+q, lane l) owns feature row r = 32q+l of
 // the tile = TMEM lane r; in atom a its 16-byte chunk c sits at a*16K + r*128 + ((c ^ (r & 7)) << 4),
 // so a warp's 128-bit loads are bank-conflict free.
+// Gate tiles (kGateTask, FP32 config) stream token rows through the same converter path; the
+// converters also accumulate each token row's sum of squares into gate_na (certified-gate bound).
 template <int PREC>
 __device__ void gemm_wconvert(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, unsigned long long* trace,
-                              unsigned long long* clog) {
+                              unsigned long long* clog, double* gate_na = nullptr) {
     using Cfg = GemmCfg<PREC>;
     long long w_w = 0, w_a = 0;
     int nlog = 0;
@@ -1414,6 +1436,8 @@ __device__ void gemm_wconvert(const LaunchParams& P, uint8_t* ring, GemmCtrl& G,
     while (true) {
         if (!mbar_wait(&G.qfull[q], qphase, P.abort_flag)) return;
         const int type = G.ring[q].type;
+        const int g_tok0 = G.ring[q].m, g_valid = G.ring[q].cnt[0];
+        const bool g_norm = type == kGateTask && G.ring[q].nb == 0 && gate_na != nullptr;
         __syncwarp();
         if (lane == 0) mbar_arrive(&G.qempty[q]);
         if (++q == kTaskRing) { q = 0; qphase ^= 1u; }
@@ -1421,7 +1445,8 @@ __device__ void gemm_wconvert(const LaunchParams& P, uint8_t* ring, GemmCtrl& G,
             if (threadIdx.x == kWarpConv0 * 32 && trace) { trace[kWaitConvW] = w_w; trace[kWaitConvA] = w_a; }
             return;
         }
-        const int nk = ((type == 0 ? P.H : P.D) + Cfg::BK - 1) / Cfg::BK;
+        const int nk = (task_k(P, type) + Cfg::BK - 1) / Cfg::BK;
+        double ss = 0.0;   // gate tile: sum of squares of this row (float per stage, double across stages)
         for (int kb = 0; kb < nk; ++kb) {
             const long long c0 = clk();
             if (!FD_TIMED_WAIT(w_w, mbar_wait(&G.wfull[wst], wphase, P.abort_flag))) return;
@@ -1433,11 +1458,29 @@ __device__ void gemm_wconvert(const LaunchParams& P, uint8_t* ring, GemmCtrl& G,
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
                     c[at][i] = *reinterpret_cast<const float4*>(wrow + at * Cfg::ATOM_BYTES + ((i ^ (r & 7)) << 4));
+            // the slot is refilled by the async proxy (TMA) as soon as it is released: order these generic
+            // loads before that write (without the fence the release can retire before the loaded data
+            // returns, and a TMA issued right behind it corrupts rows of this stage -- seen on the gate's
+            // second tile, tools/dev/gate_stage_dump.py)
+            fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(&G.wempty[wst]);   // values are in registers: slot reusable
             if (++wst == Cfg::WSTAGES) { wst = 0; wphase ^= 1u; }
 
             const long long c2 = clk();
+            if (PREC == kFP32 && g_norm) {
+                float cs = 0.0f;
+#pragma unroll
+                for (int at = 0; at < Cfg::NATOM; ++at)
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const float4 v = c[at][i];
+                        cs = __fmaf_rn(v.x, v.x, cs); cs = __fmaf_rn(v.y, v.y, cs);
+                        cs = __fmaf_rn(v.z, v.z, cs); cs = __fmaf_rn(v.w, v.w, cs);
+                    }
+                ss += (double)cs;
+                if (kb + 1 == nk && r < g_valid) gate_na[g_tok0 + r] = ss;
+            }
             if constexpr (PREC == kFP32) {
                 // one TMEM half-stage per 128-byte atom (32 K values: hi columns [0, 32), lo [32, 64)),
                 // each released to the MMA warp on its own so the ring runs half a stage ahead
@@ -1553,23 +1596,21 @@ __device__ __forceinline__ void issue_stage(uint32_t d_tmem, uint32_t abase, uin
 // CORR_FIRST: corrections then main (back-to-back MMAs never read the same TMEM A columns either way).
 template <bool MAIN, bool CORR>
 __device__ __forceinline__ void issue_half_fp32(uint32_t d_main, uint32_t d_corr, uint32_t a_half, uint64_t bdesc,
-                                                uint32_t main_acc, uint32_t corr_acc) {
+                                                uint32_t idesc, uint32_t main_acc, uint32_t corr_acc) {
     using Cfg = GemmCfg<kFP32>;
     if (CORR) {
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks)   // w_lo * x_hi
-            mma_tf32_ts(d_corr, a_half + Cfg::ATOM_K + ks * Cfg::KSTEP, bdesc + ((ks * 32) >> 4),
-                        Cfg::IDESC, ks == 0 ? corr_acc : 1u);
+            mma_tf32_ts(d_corr, a_half + Cfg::ATOM_K + ks * Cfg::KSTEP, bdesc + ((ks * 32) >> 4), idesc,
+                        ks == 0 ? corr_acc : 1u);
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks)   // w_hi * x_lo
-            mma_tf32_ts(d_corr, a_half + ks * Cfg::KSTEP,
-                        bdesc + ((Cfg::PLANE_BYTES + ks * 32) >> 4), Cfg::IDESC, 1u);
+            mma_tf32_ts(d_corr, a_half + ks * Cfg::KSTEP, bdesc + ((Cfg::PLANE_BYTES + ks * 32) >> 4), idesc, 1u);
     }
     if (MAIN) {
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks)   // w_hi * x_hi
-            mma_tf32_ts(d_main, a_half + ks * Cfg::KSTEP, bdesc + ((ks * 32) >> 4), Cfg::IDESC,
-                        ks == 0 ? main_acc : 1u);
+            mma_tf32_ts(d_main, a_half + ks * Cfg::KSTEP, bdesc + ((ks * 32) >> 4), idesc, ks == 0 ? main_acc : 1u);
     }
 }
 
@@ -1583,7 +1624,8 @@ struct MmaFp32State {
 // fold of the previous tile: cempty). The tile's first half-stage issues its main MMAs before waiting
 // for the fold, so the fold overlaps them.
 __device__ __forceinline__ bool mma_tile_fp32(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, uint32_t tmem,
-                                              uint32_t d_main, int nk, MmaFp32State& st, long long& w_x) {
+                                              uint32_t d_main, int nk, uint32_t idesc, MmaFp32State& st,
+                                              long long& w_x) {
     using Cfg = GemmCfg<kFP32>;
     const uint32_t d_corr = tmem + kTmemCorr;
     for (int kb = 0; kb < nk; ++kb) {
@@ -1597,19 +1639,62 @@ __device__ __forceinline__ bool mma_tile_fp32(const LaunchParams& P, uint8_t* ri
             const uint32_t a_half = tmem + Cfg::TMEM_A0 + st.ah * Cfg::A_COLS;
             const uint64_t bd = bdesc + ((at * Cfg::ATOM_BYTES) >> 4);
             if (kb == 0 && at == 0) {
-                issue_half_fp32<true, false>(d_main, d_corr, a_half, bd, 0u, 0u);
+                issue_half_fp32<true, false>(d_main, d_corr, a_half, bd, idesc, 0u, 0u);
                 if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.cempty, st.cph ^ 1u, P.abort_flag))) return false;
                 st.cph ^= 1u;
                 tc_fence_after();
-                issue_half_fp32<false, true>(d_main, d_corr, a_half, bd, 0u, 0u);
+                issue_half_fp32<false, true>(d_main, d_corr, a_half, bd, idesc, 0u, 0u);
             } else {
-                issue_half_fp32<true, true>(d_main, d_corr, a_half, bd, 1u, 1u);
+                issue_half_fp32<true, true>(d_main, d_corr, a_half, bd, idesc, 1u, 1u);
             }
             mma_commit(&G.aempty[st.ah]);
             if (++st.ah == Cfg::A_SLOTS) { st.ah = 0; st.ahph ^= 1u; }
         }
         mma_commit(&G.done[st.stage]);
         if (++st.stage == Cfg::STAGES) { st.stage = 0; st.phase ^= 1u; }
+    }
+    return true;
+}
+
+// Gate tile (kGateTask): the main (w_hi x_hi) products of every 64-K stage go to a fresh accumulator
+// (ping-pong acc[0]/acc[1], tfull after each stage), which the gate epilogue folds into registers in
+// round-to-nearest FP32: each accumulator then sees only 8 truncating MMAs on a 64-term partial sum, and
+// the epilogue gets the chunk-end prefix sums the certificate needs (gate_epilogue). The corrections
+// accumulate over the whole tile in kTmemCorr as in the FFN.
+__device__ __forceinline__ bool mma_gate_tile(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, uint32_t tmem, int nk,
+                                              uint32_t idesc, MmaFp32State& st, int& acc, uint32_t& accphase,
+                                              long long& w_x) {
+    using Cfg = GemmCfg<kFP32>;
+    const uint32_t d_corr = tmem + kTmemCorr;
+    for (int kb = 0; kb < nk; ++kb) {
+        if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.tempty[acc], accphase ^ 1u, P.abort_flag))) return false;
+        const uint32_t d_main = tmem + (uint32_t)(acc * kNT);
+        if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.ready[st.stage], st.phase, P.abort_flag))) return false;
+        tc_fence_after();
+        const uint64_t bdesc = umma_desc_kmajor(smem_u32(ring + st.stage * Cfg::STAGE_BYTES), 128);
+#pragma unroll
+        for (int at = 0; at < Cfg::NATOM; ++at) {
+            if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.afull[st.ah], st.ahph, P.abort_flag))) return false;
+            tc_fence_after();
+            const uint32_t a_half = tmem + Cfg::TMEM_A0 + st.ah * Cfg::A_COLS;
+            const uint64_t bd = bdesc + ((at * Cfg::ATOM_BYTES) >> 4);
+            const uint32_t main_acc = at == 0 ? 0u : 1u;
+            if (kb == 0 && at == 0) {
+                issue_half_fp32<true, false>(d_main, d_corr, a_half, bd, idesc, 0u, 0u);
+                if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.cempty, st.cph ^ 1u, P.abort_flag))) return false;
+                st.cph ^= 1u;
+                tc_fence_after();
+                issue_half_fp32<false, true>(d_main, d_corr, a_half, bd, idesc, 0u, 0u);
+            } else {
+                issue_half_fp32<true, true>(d_main, d_corr, a_half, bd, idesc, main_acc, 1u);
+            }
+            mma_commit(&G.aempty[st.ah]);
+            if (++st.ah == Cfg::A_SLOTS) { st.ah = 0; st.ahph ^= 1u; }
+        }
+        mma_commit(&G.done[st.stage]);
+        if (++st.stage == Cfg::STAGES) { st.stage = 0; st.phase ^= 1u; }
+        mma_commit(&G.tfull[acc]);   // this stage's main partial (and, at the last stage, the corrections)
+        if (++acc == kAccStages) { acc = 0; accphase ^= 1u; }
     }
     return true;
 }
@@ -1644,11 +1729,19 @@ __device__ void gemm_mma(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, unsi
             return;
         }
         ++ntile;
-        const int nk = ((type == 0 ? P.H : P.D) + Cfg::BK - 1) / Cfg::BK;
+        const int nk = (task_k(P, type) + Cfg::BK - 1) / Cfg::BK;
+        if constexpr (PREC == kFP32) {
+            if (type == kGateTask) {
+                if (!mma_gate_tile(P, ring, G, tmem, nk, umma_idesc(2u, kBF, (uint32_t)P.gate_n), st32, acc, accphase,
+                                   w_x))
+                    return;
+                continue;
+            }
+        }
         if (!FD_TIMED_WAIT(w_acc, mbar_wait(&G.tempty[acc], accphase ^ 1u, P.abort_flag))) return;
         const uint32_t d_tmem = tmem + (uint32_t)(acc * kNT);
         if constexpr (PREC == kFP32) {
-            if (!mma_tile_fp32(P, ring, G, tmem, d_tmem, nk, st32, w_x)) return;
+            if (!mma_tile_fp32(P, ring, G, tmem, d_tmem, nk, Cfg::IDESC, st32, w_x)) return;
             mma_commit(&G.tfull[acc]);   // main + correction accumulators ready for the epilogue
             if (++acc == kAccStages) { acc = 0; accphase ^= 1u; }
             continue;
@@ -1974,6 +2067,148 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
     }
 }
 
+// ================================================================ phase 1a: gate logits on the tensor cores
+// The gate GEMM z~ = A Wg of this CTA's token range runs through the FFN pipeline roles in the FP32
+// (3xTF32) configuration with the operands in the other roles: the token rows (raw FP32, TMA from the
+// caller's shard) take the weight role (converter warps split them into tf32 hi/lo TMEM operands and
+// accumulate each row's sum of squares), the pre-split Wg^T hi/lo planes take the token role (smem
+// B operand, N = gate_n experts per block). One task per (128-token tile, expert block).
+__device__ void gate_producer(const LaunchParams& P, const RankCtx& R, int rl, uint8_t* ring, GemmCtrl& G,
+                              int tokA, int tokB) {
+    using Cfg = GemmCfg<kFP32>;
+    int stage = 0, wstage = 0, q = 0;
+    uint32_t phase = 0, wphase = 0, qphase = 0;
+    const CUtensorMap* ta = &P.tm_in[rl];
+    tma_prefetch(ta);
+    tma_prefetch(&R.tm_wg[0]);
+    tma_prefetch(&R.tm_wg[1]);
+    const uint64_t pol = l2_policy_evict_last();   // token rows: re-read by the dispatch push; Wg: by every CTA
+    const int nk = (P.H + Cfg::BK - 1) / Cfg::BK;
+    const uint32_t bbytes = (uint32_t)(Cfg::PLANES * Cfg::NATOM * P.gate_n * 128);
+    for (int tok0 = tokA; tok0 < tokB; tok0 += kNT)
+        for (int eb = 0; eb < P.gate_nblk; ++eb) {
+            if (!mbar_wait(&G.qempty[q], qphase ^ 1u, P.abort_flag)) return;
+            Task tk{};
+            tk.type = kGateTask;
+            tk.m = tok0;
+            tk.nb = eb;
+            tk.nsrc = 1;
+            tk.cnt[0] = min(kNT, tokB - tok0);
+            G.ring[q] = tk;
+            mbar_arrive(&G.qfull[q]);
+            if (++q == kTaskRing) { q = 0; qphase ^= 1u; }
+            for (int kb = 0; kb < nk; ++kb) {
+                if (!mbar_wait(&G.wempty[wstage], wphase ^ 1u, P.abort_flag)) return;
+                mbar_expect_tx(&G.wfull[wstage], Cfg::W_BYTES);
+#pragma unroll
+                for (int at = 0; at < Cfg::NATOM; ++at)
+                    tma_load_2d_hint(ring + Cfg::W_OFF + wstage * Cfg::W_BYTES + at * Cfg::ATOM_BYTES, ta,
+                                     &G.wfull[wstage], kb * Cfg::BK + at * Cfg::ATOM_K, tok0, pol);
+                if (++wstage == Cfg::WSTAGES) { wstage = 0; wphase ^= 1u; }
+                if (!mbar_wait(&G.done[stage], phase ^ 1u, P.abort_flag)) return;
+                uint8_t* st = ring + stage * Cfg::STAGE_BYTES;
+                mbar_expect_tx(&G.ready[stage], bbytes);
+#pragma unroll
+                for (int pl = 0; pl < Cfg::PLANES; ++pl)
+#pragma unroll
+                    for (int at = 0; at < Cfg::NATOM; ++at)
+                        tma_load_2d_hint(st + pl * Cfg::PLANE_BYTES + at * Cfg::ATOM_BYTES, &R.tm_wg[pl], &G.ready[stage],
+                                         kb * Cfg::BK + at * Cfg::ATOM_K, eb * P.gate_n, pol);
+                if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
+            }
+        }
+    if (!mbar_wait(&G.qempty[q], qphase ^ 1u, P.abort_flag)) return;
+    G.ring[q].type = -1;
+    mbar_arrive(&G.qfull[q]);
+}
+
+// warps 4-7: thread = TMEM lane = token row of the tile. Per 64-K stage it adds the stage's main partial
+// (gate_n <= 128 expert columns) into z[] in round-to-nearest FP32 and accumulates
+//   sab += max_e |z_e|   (the prefix sums at 64-term chunk ends: the certificate's Sab, gate.hpp:77-81 chain)
+// then adds the corrections at the end and writes the z~ row to g_phi and Sab to gate_sab (the certified
+// routing reads both back; it overwrites g_phi with probabilities).
+__device__ void gate_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl& G) {
+    using Cfg = GemmCfg<kFP32>;
+    const int et = threadIdx.x - kWarpEpi0 * 32;
+    const uint32_t lanes = (uint32_t)((et >> 5) * 32) << 16;
+    const uint32_t tmem = G.tmem_base;
+    const int nk = (P.H + Cfg::BK - 1) / Cfg::BK;
+    int q = 0, acc = 0;
+    uint32_t qphase = 0, accphase = 0;
+    while (true) {
+        if (!mbar_wait(&G.qfull[q], qphase, P.abort_flag)) return;
+        const int type = G.ring[q].type, tok0 = G.ring[q].m, eb = G.ring[q].nb, valid = G.ring[q].cnt[0];
+        if (type < 0) return;
+        const int e0 = eb * P.gate_n;
+        const int nv = min(P.gate_n, P.E - e0);   // valid expert columns of this block
+        float z[kBF];
+#pragma unroll
+        for (int i = 0; i < kBF; ++i) z[i] = 0.0f;
+        float sab = 0.0f;
+        for (int kb = 0; kb < nk; ++kb) {
+            if (!mbar_wait(&G.tfull[acc], accphase, P.abort_flag)) return;
+            tc_fence_after();
+            float m = 0.0f;
+#pragma unroll
+            for (int ch = 0; ch < kBF / 16; ++ch) {
+                if (ch * 16 < P.gate_n) {
+                    uint32_t v[16];
+                    tmem_ld16(tmem + lanes + (uint32_t)(acc * kNT + ch * 16), v);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        z[ch * 16 + i] = __fadd_rn(z[ch * 16 + i], __uint_as_float(v[i]));
+                        if (ch * 16 + i < nv) m = fmaxf(m, fabsf(z[ch * 16 + i]));
+                    }
+                }
+            }
+            sab = __fadd_ru(sab, m);
+            tc_fence_before();
+            __syncwarp();
+            if ((et & 31) == 0) mbar_arrive(&G.tempty[acc]);
+            if (++acc == kAccStages) { acc = 0; accphase ^= 1u; }
+        }
+        // the last stage's tfull also covered every correction MMA of the tile
+#pragma unroll
+        for (int ch = 0; ch < kBF / 16; ++ch) {
+            if (ch * 16 < P.gate_n) {
+                uint32_t v[16];
+                tmem_ld16(tmem + lanes + kTmemCorr + (uint32_t)(ch * 16), v);
+                tmem_wait_ld();
+#pragma unroll
+                for (int i = 0; i < 16; ++i) z[ch * 16 + i] = __fadd_rn(z[ch * 16 + i], __uint_as_float(v[i]));
+            }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if ((et & 31) == 0) mbar_arrive(&G.cempty);
+        if (et < valid) {
+            float* zrow = R.g_phi + (size_t)(tok0 + et) * P.E + e0;
+#pragma unroll
+            for (int i = 0; i < kBF; ++i)
+                if (i < nv) zrow[i] = z[i];
+            int* sp = reinterpret_cast<int*>(R.gate_sab) + tok0 + et;
+            if (eb == 0) *sp = __float_as_int(sab);
+            else atomicMax(sp, __float_as_int(sab));   // non-negative floats order like their bits
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (et == 0) mbar_arrive(&G.qempty[q]);
+        if (++q == kTaskRing) { q = 0; qphase ^= 1u; }
+    }
+}
+
+__device__ __forceinline__ void init_ctrl_fp32(GemmCtrl& G, uint32_t tmem_base, uint32_t tempty_count) {
+    using Cfg = GemmCfg<kFP32>;
+    for (int i = 0; i < Cfg::STAGES; ++i) { mbar_init(&G.ready[i], ReadyCount<kFP32>::N); mbar_init(&G.done[i], 1); }
+    for (int i = 0; i < Cfg::WSTAGES; ++i) { mbar_init(&G.wfull[i], 1); mbar_init(&G.wempty[i], 4); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&G.afull[i], 4); mbar_init(&G.aempty[i], 1); }
+    mbar_init(&G.cempty, 4);
+    for (int i = 0; i < kAccStages; ++i) { mbar_init(&G.tfull[i], 1); mbar_init(&G.tempty[i], tempty_count); }
+    for (int i = 0; i < kTaskRing; ++i) { mbar_init(&G.qfull[i], 1); mbar_init(&G.qempty[i], kTaskConsumers); }
+    for (int i = 0; i < kTaskRing; ++i) { mbar_init(&G.sfull[i], 1); mbar_init(&G.sempty[i], 1); }
+    G.tmem_base = tmem_base;
+}
+
 // ================================================================ phase 4: combine
 static_assert(kCombineTok == kGateTok, "combine tasks are aligned with gate blocks (blk_ready)");
 // O[t] = sum over the token's kept picks, in pick order, of w * y (oracle.hpp:102-107): one warp
@@ -2117,7 +2352,31 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
     tc_fence_after();
     const uint32_t tmem_base = G.tmem_base;
 
-    // phase 1: exact gate (uses the smem region as scratch)
+    // phase 1a: gate logits on the tensor cores (FP32 pipeline roles, own control block)
+    if (P.gate_tc) {
+        GemmCtrl& GG = *reinterpret_cast<GemmCtrl*>(smem + SmemPlan<PREC>::CTRL_GATE);
+        if (tid == 0) {
+            init_ctrl_fp32(GG, tmem_base, 4);   // gate epilogue: one tempty arrival per warp per stage
+            mbar_fence_init();
+        }
+        __syncthreads();
+        int tokA, tokB, b0, b1;
+        gate_token_range(P, cta, tokA, tokB, b0, b1);
+        if (warp == kWarpMma) {
+            if ((tid & 31) == 0) gemm_mma<kFP32>(P, ring, GG, trace, nullptr);
+        } else if (warp == kWarpProducer) {
+            if ((tid & 31) == 0) gate_producer(P, R, rl, ring, GG, tokA, tokB);
+        } else if (warp >= kWarpConv0 && warp < kWarpConv0 + 4) {
+            gemm_wconvert<kFP32>(P, ring, GG, nullptr, nullptr, R.gate_na);
+        } else if (warp >= kWarpEpi0 && warp < kWarpEpi0 + 4) {
+            gate_epilogue(P, R, GG);
+        }
+        tc_fence_before();
+        __syncthreads();
+        tc_fence_after();
+        if (tid == 0) trace[kTrGateTc] = globaltimer();
+    }
+    // phase 1b: routing (certified from the tensor-core logits, or the SIMT gate), smem region as scratch
     gate_phase(P, R, A, cta, smem, s_stat);
     if (tid == 0) {
         trace[1] = globaltimer();
@@ -2287,7 +2546,7 @@ __global__ void __launch_bounds__(kThreads, 1) debug_gemm_kernel(const __grid_co
             P.abort_flag = abort_flag;
             MmaFp32State st;
             long long w = 0;
-            mma_tile_fp32(P, smem, G, tmem, tmem, nk, st, w);
+            mma_tile_fp32(P, smem, G, tmem, tmem, nk, GemmCfg<kFP32>::IDESC, st, w);
         } else {
             int stage = 0; uint32_t phase = 0;
             for (int kb = 0; kb < nk; ++kb) {

@@ -34,6 +34,7 @@ size_t align_up(size_t x, size_t a = kAlign) { return (x + a - 1) / a * a; }
 struct Dims {
     int64_t S, H, D, E, El, P, k, C, Cp, RP, MT, RBF, NB0, NB1;
     int64_t rows_x, rows_w1, rows_w2;
+    int64_t gate_n, gate_nblk;      // tensor-core gate: experts per MMA block (N), blocks
     int prec, esz, planes;
 };
 
@@ -56,6 +57,8 @@ Dims make_dims(const fdmoe_config& c) {
     d.rows_x = std::max(d.El * d.RP, (d.El - 1) * d.RP + d.MT * kBM);
     d.rows_w1 = (d.El - 1) * d.D + d.NB0 * kBF;
     d.rows_w2 = (d.El - 1) * d.H + d.NB1 * kBF;
+    d.gate_n = d.E <= kBF ? (d.E + 15) / 16 * 16 : kBF;
+    d.gate_nblk = (d.E + d.gate_n - 1) / d.gate_n;
     d.prec = c.precision;
     d.esz = c.precision == FDMOE_FP32 ? 4 : 2;
     d.planes = c.precision == FDMOE_FP32 ? 2 : 1;
@@ -105,6 +108,9 @@ struct RankRes {
     void* w1[2] = {nullptr, nullptr};
     void* w2[2] = {nullptr, nullptr};
     float *b1 = nullptr, *b2 = nullptr, *wg = nullptr, *wg_norm = nullptr, *wgT = nullptr;
+    float* wg_split = nullptr;      // tensor-core gate: Wg^T tf32 hi plane, then lo plane, [gate_nblk*gate_n][H] each
+    double* gate_na = nullptr;      // [S] token-row sums of squares (tensor-core gate)
+    float* gate_sab = nullptr;      // [S] certificate chunk-end prefix sums (tensor-core gate)
     float* g_phi = nullptr;
     int32_t *pick_e = nullptr, *pick_slot = nullptr;
     float* pick_w = nullptr;
@@ -212,6 +218,9 @@ fdmoe_status alloc_rank(fdmoe_handle* h, RankRes& r, int ctas_per_rank) {
     parts.push_back({(void**)&r.wg, (size_t)d.H * d.E * 4});
     parts.push_back({(void**)&r.wg_norm, (size_t)d.E * 4});
     parts.push_back({(void**)&r.wgT, (size_t)d.E * d.H * 4});
+    parts.push_back({(void**)&r.wg_split, (size_t)2 * d.gate_nblk * d.gate_n * d.H * 4});
+    parts.push_back({(void**)&r.gate_na, (size_t)d.S * 8});
+    parts.push_back({(void**)&r.gate_sab, (size_t)d.S * 4});
     parts.push_back({(void**)&r.g_phi, (size_t)d.S * d.E * 4});
     parts.push_back({(void**)&r.pick_e, (size_t)d.S * d.k * 4});
     parts.push_back({(void**)&r.pick_slot, (size_t)d.S * d.k * 4});
@@ -265,11 +274,17 @@ fdmoe_status build_ctx(fdmoe_handle* h) {
             }
             if ((st = make_tmap(&c.tm_w1, r.w1[0], d.rows_w1, d.H, d.esz, kBF))) return st;
             if ((st = make_tmap(&c.tm_w2, r.w2[0], d.rows_w2, d.D, d.esz, kBF))) return st;
+            for (int pl = 0; pl < 2; ++pl)
+                if ((st = make_tmap(&c.tm_wg[pl], r.wg_split + (size_t)pl * d.gate_nblk * d.gate_n * d.H,
+                                    d.gate_nblk * d.gate_n, d.H, 4, (int)d.gate_n)))
+                    return st;
             for (int q = 0; q < d.P; ++q) c.peer_heap[q] = r.peer[q];
             c.hl = r.hl;
             c.c1[0] = r.c1[0];
             c.c1[1] = r.c1[d.planes - 1];
             c.b1 = r.b1; c.b2 = r.b2; c.wg = r.wg; c.wg_norm = r.wg_norm; c.wgT = r.wgT;
+            c.gate_na = r.gate_na;
+            c.gate_sab = r.gate_sab;
             c.g_phi = r.g_phi; c.pick_e = r.pick_e; c.pick_slot = r.pick_slot; c.pick_w = r.pick_w;
             c.cnt_cta = r.cnt_cta; c.tbl_tok = r.tbl_tok; c.tbl_w = r.tbl_w; c.slot_counts = r.slot_counts;
             c.blk_ready = r.blk_ready;
@@ -485,7 +500,7 @@ fdmoe_status fdmoe_set_weights(fdmoe_handle* h, const float* wg, const float* w1
     const Dims& d = h->dm;
     const cudaMemcpyKind kind = where == FDMOE_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
     // |Wg[:, e]|_2 for the certified gate, computed in double and rounded up to float
-    std::vector<float> wn(d.E), wt((size_t)d.E * d.H);
+    std::vector<float> wn(d.E), wt((size_t)d.E * d.H), wsplit;
     {
         std::vector<float> hw;
         const float* src = wg;
@@ -499,6 +514,21 @@ fdmoe_status fdmoe_set_weights(fdmoe_handle* h, const float* wg, const float* w1
             for (int64_t e = 0; e < d.E; ++e) {
                 ss[e] += (double)src[x * d.E + e] * src[x * d.E + e];
                 wt[e * d.H + x] = src[x * d.E + e];
+            }
+        // tensor-core gate operand: Wg^T split into a tf32 hi plane (round to nearest, as tf32_hi on the
+        // device) and the exact remainder plane; expert rows past E are zero
+        const size_t plane = (size_t)d.gate_nblk * d.gate_n * d.H;
+        wsplit.assign(2 * plane, 0.0f);
+        for (int64_t e = 0; e < d.E; ++e)
+            for (int64_t x = 0; x < d.H; ++x) {
+                const float v = wt[e * d.H + x];
+                uint32_t u;
+                std::memcpy(&u, &v, 4);
+                u = (u + 0x1000u) & 0xFFFFE000u;
+                float hi;
+                std::memcpy(&hi, &u, 4);
+                wsplit[e * d.H + x] = hi;
+                wsplit[plane + e * d.H + x] = v - hi;
             }
         for (int64_t e = 0; e < d.E; ++e) {
             const double n = std::sqrt(ss[e]) * (1.0 + 1e-12);
@@ -525,6 +555,7 @@ fdmoe_status fdmoe_set_weights(fdmoe_handle* h, const float* wg, const float* w1
         CK(cudaMemcpy(r.wg, wg, (size_t)d.H * d.E * 4, kind));
         CK(cudaMemcpy(r.wg_norm, wn.data(), (size_t)d.E * 4, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(r.wgT, wt.data(), wt.size() * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(r.wg_split, wsplit.data(), wsplit.size() * 4, cudaMemcpyHostToDevice));
     }
     h->weights_set = true;
     return FDMOE_OK;
@@ -580,6 +611,30 @@ static fdmoe_status launch_all(fdmoe_handle* h, const float* const* in_dev, floa
             const double u = std::ldexp(1.0, -24), n1 = (double)d.H + 1.0;
             p.gate_u = (float)(u * 1.001);
             p.gate_k1 = (float)((66.0 + 2.0 * (double)d.H * (n1 * u / (1.0 - n1 * u))) * 1.001);
+        }
+        {   // tensor-core gate (fdmoe_kernel.cu phase 1a): 3xTF32 logits folded per 64-K chunk, certified with
+            //   |z~ - z_ref| <= u' (64 Sab + k1_tc |a| |w_e|)
+            // The reference chain (gate.hpp:77-81): u sum_i |s_i| + u sum |a_x w_x|, with |s_i| <= |P_J-1| + S_J inside
+            // chunk J (P: prefix at chunk ends, S_J = sum over the chunk of |a_x w_x|), so <= u (64 Sab + 65 |a||w|)
+            // (+ 2H gamma_{H+1} |a||w| for computed-vs-exact partials, + 1 for Sab's own error). Ours: tf32 products
+            // 2^-19 = 32u; per 64-K chunk 8 main MMAs, each < 3 ulp of the chunk's magnitude (products truncated 2
+            // bits below the accumulator's ulp + final round toward zero: tools/dev/acc_guard.py) -> 48u sum S_J;
+            // <= 2H/64 register folds (u each); the 2^-9-scaled correction accumulator (2H/8 MMAs) -> 6u; the
+            // corrections' fold u. All terms times |a||w_e| >= sum |a_x||w_xe|.
+            bool aligned = true;
+            for (size_t i = 0; i < g.members.size(); ++i) aligned &= ((uintptr_t)p.in[i] & 15u) == 0;
+            p.gate_tc = (!p.exact_gate && aligned) ? 1 : 0;
+            p.gate_n = (int)d.gate_n;
+            p.gate_nblk = (int)d.gate_nblk;
+            const double u = std::ldexp(1.0, -24), H = (double)d.H, n1 = H + 1.0;
+            const double chunks = std::ceil(H / 64.0);
+            p.gate_k1_tc = (float)((65.0 + 2.0 * H * (n1 * u / (1.0 - n1 * u)) + 1.0 + 32.0 + 48.0 + chunks + 6.0 + 1.0 +
+                                    8.0) * 1.001);
+            if (p.gate_tc)
+                for (size_t i = 0; i < g.members.size(); ++i) {
+                    fdmoe_status ts = make_tmap(&p.tm_in[i], p.in[i], d.S, d.H, 4, kNT);
+                    if (ts) return ts;
+                }
         }
         const char* dbg = getenv("FDMOE_DEBUG");   // ablation switches (tools/ablate.py); unset in production
         p.debug = dbg ? atoi(dbg) : 0;
