@@ -185,6 +185,7 @@ def main():
     ap.add_argument("--experts", type=int, default=E_TOTAL)
     ap.add_argument("--e2e-steps", type=int, default=12)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-bulksync", action="store_true")
     args = ap.parse_args()
     assert args.warmup >= 3, "timing rules: at least 3 warm-up steps"
 
@@ -255,6 +256,10 @@ def main():
         my = shards_all
     op.set_weights(model)
     info = op.info()
+    bulk = None
+    if not args.no_bulksync:
+        from paper_2506_04667_b200.bulksync import BulkSyncMoE
+        bulk = BulkSyncMoE(cfg, model, rank=rank if world > 1 else 0, world=world if world > 1 else 1)
     del model
     setup_s = time.perf_counter() - t_setup
 
@@ -313,6 +318,27 @@ def main():
     seq_ms = ev0.elapsed_time(ev1) / seq_steps
     if world > 1:
         seq_ms = fdist.max_over_ranks(seq_ms, device="cuda")
+
+    # ---------------------------------------------------------------- bulk-synchronous NCCL baseline (§8 f1)
+    # separate library kernels + NCCL all_to_all_single for dispatch and combine (bulksync.py): the
+    # conventional schedule the single fused launch replaces (runtime.hpp:885-908)
+    bulk_ms = None
+    if bulk is not None and n == (world if world > 1 else 1):
+        xin = ins[0]
+        for _ in range(2):
+            bulk.forward(xin)
+        torch.cuda.synchronize()
+        barrier()
+        ev0.record(stream)
+        for _ in range(seq_steps):
+            bulk.forward(xin)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        bulk_ms = ev0.elapsed_time(ev1) / seq_steps
+        if world > 1:
+            bulk_ms = fdist.max_over_ranks(bulk_ms, device="cuda")
+        del bulk
+        torch.cuda.empty_cache()
 
     # ---------------------------------------------------------------- end to end through the C ABI (host buffers)
     pinned = [torch.from_numpy(s).pin_memory() for s in my]
@@ -393,8 +419,12 @@ def main():
             "clocks": clk.summary(), "setup_s": setup_s, "operator_event_ms_last_launch": st_ms,
             "operator": {k: info[k] for k in ("capacity", "packet_rows", "ctas_per_rank", "smem_bytes")},
             "schedules": {"overlapped_ms": ms, "sequential_ms": seq_ms, "sequential_over_overlapped": seq_ms / ms,
+                          "sequential_nccl_ms": bulk_ms,
+                          "sequential_nccl_over_overlapped": (bulk_ms / ms) if bulk_ms else None,
                           "note": "sequential = ScheduleMode::sequential in the same single launch (group "
-                                  "barriers after dispatch and after the FFN); not timed steps of `value`"}}
+                                  "barriers after dispatch and after the FFN); sequential_nccl = bulk-synchronous "
+                                  "separate kernels (cuBLAS FP32 SGEMM, TF32 off) + NCCL all_to_all_single for "
+                                  "dispatch and combine (bulksync.py); neither is a timed step of `value`"}}
     if rank == 0 and not args.no_cpu_baseline:
         try:
             budget = 15.0

@@ -122,11 +122,56 @@ EXPORTED_SYMBOLS = [
     "fdmoe_gemm_tasks_for_rows", "fdmoe_combine_tiles_for_rows", "fdmoe_initial_task_bound",
     "fdmoe_synth_model", "fdmoe_synth_shards", "fdmoe_create", "fdmoe_destroy", "fdmoe_ipc_size",
     "fdmoe_export_heap", "fdmoe_import_peers", "fdmoe_set_weights", "fdmoe_forward", "fdmoe_forward_async",
-    "fdmoe_sync", "fdmoe_get_info", "fdmoe_last_kernel_ms", "fdmoe_read_trace", "fdmoe_debug_expf", "fdmoe_debug_gemm", "fdmoe_debug_mma_rate", "fdmoe_debug_latency", "fdmoe_read_chunklog",
+    "fdmoe_sync", "fdmoe_get_info", "fdmoe_last_kernel_ms", "fdmoe_read_trace",
     "fdmoe_read_events", "fdmoe_straggler_delays", "fdmoe_forward_stream",
 ]
 
 _LIB = None
+_DEV_LIB = None
+_LIB_PATH = None   # select_library(): tools/ A/B runs of another build; None = the in-tree product library
+
+
+def select_library(path: str):
+    """Tools only: run the operator on another build of the library (e.g. lib/libfdmoe_dev.so for the
+    FDMOE_DEBUG ablations and wait accounting, or an A/B build). Must precede the first lib() call."""
+    global _LIB_PATH
+    if _LIB is not None:
+        raise RuntimeError("select_library() after the library was loaded")
+    _LIB_PATH = path
+
+
+def _load(path: str):
+    if path in (_build.LIB, _build.DEV_LIB) and (not os.path.exists(path) or _build._stale(path)):
+        try:
+            _build.build()
+        except Exception as e:  # no nvcc on a deployment box: the prebuilt .so must exist
+            if not os.path.exists(path):
+                raise ImportError(f"{os.path.basename(path)} missing and build failed: {e}") from e
+    return C.CDLL(path)
+
+
+def dev_lib():
+    """libfdmoe_dev.so: the include/fdmoe_dev.h diagnostics (device expf, single-tile GEMM, microbenchmarks)."""
+    global _DEV_LIB
+    if _DEV_LIB is None:
+        L = _load(_build.DEV_LIB)
+        vp, i32, i64, f32p = C.c_void_p, C.c_int32, C.c_int64, C.c_void_p
+        for name, (res, args) in {
+            "fdmoe_debug_expf": (i32, [f32p, f32p, i64]),
+            "fdmoe_debug_gemm": (i32, [i32, i32, f32p, f32p, f32p]),
+            "fdmoe_debug_mma_rate": (i32, [i32, i32, i32, i32, vp]),
+            "fdmoe_debug_latency": (i32, [i32, vp]),
+            "fdmoe_last_error": (C.c_char_p, []),
+        }.items():
+            fn = getattr(L, name)
+            fn.restype, fn.argtypes = res, args
+        _DEV_LIB = L
+    return _DEV_LIB
+
+
+def dev_check(status: int):
+    if status != 0:
+        raise _ERRS.get(status, FdmoeError)(dev_lib().fdmoe_last_error().decode(errors="replace"))
 
 
 def lib():
@@ -134,14 +179,8 @@ def lib():
     global _LIB
     if _LIB is not None:
         return _LIB
-    path = os.environ.get("FDMOE_LIB_OVERRIDE") or _build.LIB   # A/B experiments (tools/); unset in production
-    if path == _build.LIB and (not os.path.exists(path) or _build._stale()):
-        try:
-            _build.build()
-        except Exception as e:  # no nvcc on a deployment box: the prebuilt .so must exist
-            if not os.path.exists(path):
-                raise ImportError(f"libfdmoe.so missing and build failed: {e}") from e
-    L = C.CDLL(path)
+    path = _LIB_PATH or _build.LIB
+    L = _load(path)
     vp, i32, i64, u64, f32p = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_void_p
     sig = {
         "fdmoe_abi_version": (i32, []),
@@ -169,15 +208,12 @@ def lib():
         "fdmoe_get_info": (i32, [vp, C.POINTER(_Info)]),
         "fdmoe_last_kernel_ms": (i32, [vp, vp]),
         "fdmoe_read_trace": (i32, [vp, i32, vp, i32, vp]),
-        "fdmoe_debug_expf": (i32, [f32p, f32p, i64]),
-        "fdmoe_debug_gemm": (i32, [i32, i32, f32p, f32p, f32p]),
-        "fdmoe_debug_mma_rate": (i32, [i32, i32, i32, i32, vp]),
-        "fdmoe_debug_latency": (i32, [i32, vp]),
-        "fdmoe_read_chunklog": (i32, [vp, vp]),
         "fdmoe_read_events": (i32, [vp, i32, vp, i64, vp, vp]),
         "fdmoe_straggler_delays": (i32, [C.POINTER(_Opts), i64, i64, vp]),
         "fdmoe_forward_stream": (i32, [vp, i32, vp, vp, C.POINTER(_Opts)]),
     }
+    if hasattr(L, "fdmoe_read_chunklog"):   # development build (select_library)
+        sig["fdmoe_read_chunklog"] = (i32, [vp, vp])
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
         fn.restype = res
@@ -604,7 +640,7 @@ class Operator:
         t0 = t[:, 0].min()
         t[:, :7] -= t0
         t[:, 20:27] -= t0
-        t[:, 28] = np.where(t[:, 28] > 0, t[:, 28] - t0, 0)   # tensor-core gate logits done (0: SIMT gate)
+        t[:, 28:32] = np.where(t[:, 28:32] > 0, t[:, 28:32] - t0, 0)   # tensor-core gate logits done / staged
         return t
 
     def events(self, local_rank: int = 0) -> np.ndarray:

@@ -39,7 +39,9 @@ enum WaitSlot : int {
     kWaitMmaTask, kProdFetch, kEpiBusy, kMmaTiles,
     kTrPrefix = 20, kTrSlots, kTrSlotBarrier, kTrPush,   // dispatch sub-phases (%globaltimer)
     kTrGateLogits = 24, kTrGatePairs, kTrGateFull, kTrGateNFull,  // gate sub-phases (last sub-tile), full tokens
-    kTrGateTc = 28                                                // tensor-core gate logits done
+    kTrGateTc = 28,                                               // tensor-core gate logits done
+    kTrGateLoad = 29,                                             // tensor-core logits staged for routing
+    kTrGateDecide = 30, kTrGateExp = 31                           // thread-route decisions / exps done
 };
 
 enum Prec : int { kFP32 = 0, kBF16 = 1 };
@@ -149,7 +151,18 @@ enum DebugBits : int {
     kDbgGateNoFlush = 64, // certified gate skips the exact pass (routing wrong: timing only)
     kDbgGateNoLoad = 128, // gate skips its cp.async loads (timing only)
     kDbgGateNoMath = 256, // gate skips its dot-product loop (timing only)
+    kDbgGateNoWgTma = 512,    // tensor-core gate: producer skips the Wg^T plane TMA (timing only)
+    kDbgGateNoTokTma = 1024,  // tensor-core gate: producer skips the token-row TMA (timing only)
+    kDbgGateNoEpi = 2048,     // tensor-core gate: epilogue skips the per-stage TMEM fold (timing only)
 };
+
+// Ablation bits are honoured only by the development library (libfdmoe_dev.so, -DFDMOE_DEV);
+// the product build compiles every FD_DBG test to false.
+#ifdef FDMOE_DEV
+#define FD_DBG(bit) ((P.debug & (bit)) != 0)
+#else
+#define FD_DBG(bit) false
+#endif
 
 // Error codes written to RankCtx::err[0] (mirrors the reference's exceptions).
 enum DevErr : uint32_t { kErrNone = 0, kErrTimeout = 1, kErrProtocol = 2, kErrAccounting = 3 };

@@ -46,7 +46,9 @@ __device__ __constant__ unsigned long long c_exp_tab[32] = {
     0x3fef5818dcfba487ull, 0x3fef7c97337b9b5full, 0x3fefa4afa2a490daull, 0x3fefd0765b6e4540ull,
 };
 
-__device__ __forceinline__ float expf_glibc(float x) {
+// `tab` = the 32-entry table staged in shared memory (c_exp_tab copied by the kernel prologue): the
+// per-lane indices diverge, and divergent __constant__ loads serialise up to 32-way.
+__device__ __forceinline__ float expf_glibc(float x, const unsigned long long* __restrict__ tab) {
     const double inv_ln2_n = 0x1.71547652b82fep+0 * 32.0;
     const double shift = 0x1.8p+52;
     const double c0 = 0x1.c6af84b912394p-5 / 32.0 / 32.0 / 32.0;
@@ -65,7 +67,7 @@ __device__ __forceinline__ float expf_glibc(float x) {
     const unsigned long long ki = (unsigned long long)__double_as_longlong(kd);
     kd = __dsub_rn(kd, shift);
     const double r = __fma_rn(inv_ln2_n, xd, -kd);
-    unsigned long long t = c_exp_tab[ki & 31ull];
+    unsigned long long t = tab[ki & 31ull];
     t += ki << 47;
     const double s = __longlong_as_double((long long)t);
     const double z = __fma_rn(c0, r, c1);
@@ -286,7 +288,7 @@ constexpr int gate_region_max() {
     return m;
 }
 constexpr int kGateRegionFloats = gate_region_max();
-static_assert(kGateSubMax * 128 + 2 * kGatePairBatch * kGatePairPitch <= kGateRegionFloats, "pair buffer fits");
+static_assert(kGateSubMax * 129 + 2 * kGatePairBatch * kGatePairPitch <= kGateRegionFloats, "pair buffer fits");
 constexpr int kGateSmemBytes = ((kGateRegionFloats * 4 + 15) & ~15) + kMaxExperts * 4 /*sCnt*/ + kGateSubMax * (4 + 8 + 4 + 4 + 4) +
                                kGatePairCap * 12 + 16;
 static_assert(kGateTok <= 32, "slot assignment maps one gate block onto one warp");
@@ -329,6 +331,7 @@ struct GateSmem {
     int* sPT;        // [cap] pair token
     int* sPE;        // [cap] pair expert
     float* sPZ;      // [cap] pair exact logit
+    const unsigned long long* tab;   // glibc expf table (shared memory)
     int sub;
 };
 
@@ -361,7 +364,7 @@ __device__ void gate_logits(const LaunchParams& P, const RankCtx& R, const float
     const uint64_t pol_a = l2_policy_evict_last();   // token rows: keep for the dispatch push
     for (int base = 0; base < n_items; base += kThreads) {   // item rounds (re-stream K per round)
         auto load_stage = [&](int st, int kb) {
-            if (P.debug & kDbgGateNoLoad) { cp_async_commit(); return; }
+            if (FD_DBG(kDbgGateNoLoad)) { cp_async_commit(); return; }
             float* a = g.sA + st * g.sub * kGateApitch;
             float* w = g.sW + st * kGateKC * Ep;
             const int k0 = kb * kGateKC;
@@ -409,14 +412,14 @@ __device__ void gate_logits(const LaunchParams& P, const RankCtx& R, const float
             else cp_async_commit();
             const float* a = g.sA + st * g.sub * kGateApitch;
             const float* w = g.sW + st * kGateKC * Ep;
-            if (FAST && tid < ts && !(P.debug & kDbgGateNoNorm)) {   // |a|^2: 32-term float chunks, double sum
+            if (FAST && tid < ts && !(FD_DBG(kDbgGateNoNorm))) {   // |a|^2: 32-term float chunks, double sum
                 const float* ar = a + tid * kGateApitch;
                 float cs = 0.0f;
 #pragma unroll
                 for (int kk = 0; kk < kGateKC; ++kk) cs = __fmaf_rn(ar[kk], ar[kk], cs);
                 ss += (double)cs;
             }
-            if (active && !(P.debug & kDbgGateNoMath)) {
+            if (active && !(FD_DBG(kDbgGateNoMath))) {
                 const float* ar = a + (TT * tg) * kGateApitch;
 #pragma unroll 8
                 for (int kk = 0; kk < kGateKC; ++kk) {
@@ -481,11 +484,12 @@ __device__ __forceinline__ void warp_argmax(float& v, int& i) {
 // Routing outputs of one token from (approximate) logits in `row` with max `mx` and picks pe[0..K)
 // (one warp): G_phi and weights derive from row; expert ids are already decided.
 __device__ __forceinline__ void write_routing_from_row(const LaunchParams& P, const RankCtx& R, float* row, float mx,
-                                                       int tok, const int (&pe)[8], int* sCnt) {
+                                                       int tok, const int (&pe)[8], int* sCnt,
+                                                       const unsigned long long* g_tab) {
     const int E = P.E, K = P.k, lane = threadIdx.x & 31;
     float part = 0.0f;
     for (int e = lane; e < E; e += 32) {
-        const float x = expf_glibc(__fsub_rn(row[e], mx));
+        const float x = expf_glibc(__fsub_rn(row[e], mx), g_tab);
         row[e] = x;
         part += x;
     }
@@ -513,14 +517,15 @@ __device__ __forceinline__ void write_routing_from_row(const LaunchParams& P, co
 }
 
 // Exact routing of one token from its exact logits in `row` (one warp): gate.hpp:82-103.
-__device__ void route_exact(const LaunchParams& P, const RankCtx& R, float* row, int tok, int* sCnt) {
+__device__ void route_exact(const LaunchParams& P, const RankCtx& R, float* row, int tok, int* sCnt,
+                            const unsigned long long* tab) {
     const int E = P.E, K = P.k, lane = threadIdx.x & 31;
     // max is exact and order-free (x - max only feeds expf; +-0 ties give equal results)
     float mx = row[0];
     for (int e = lane; e < E; e += 32) mx = fmaxf(mx, row[e]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    for (int e = lane; e < E; e += 32) row[e] = expf_glibc(__fsub_rn(row[e], mx));
+    for (int e = lane; e < E; e += 32) row[e] = expf_glibc(__fsub_rn(row[e], mx), tab);
     __syncwarp();
     float sum = 0.0f;
     if (lane == 0)
@@ -672,7 +677,7 @@ __device__ int route_certified(const LaunchParams& P, const RankCtx& R, float* r
         // picks far below the max could underflow to tied zero probabilities in the reference
         ok &= prev_lb - z0 > -80.0f;
         if (ok) {
-            write_routing_from_row(P, R, row, z0, tok, pe, g.sCnt);
+            write_routing_from_row(P, R, row, z0, tok, pe, g.sCnt, g.tab);
             return 1;
         }
     }
@@ -692,6 +697,123 @@ __device__ int route_certified(const LaunchParams& P, const RankCtx& R, float* r
     if (base + n_c > kGatePairCap) return 2;
     if (lane == 0) { g.sTP0[t] = base; g.sTNC[t] = n_c; }
     return 0;
+}
+
+// Certified routing of token t by ONE thread (tensor-core logits, k <= 2, E <= 128): the decision
+// procedure of route_certified over the thread's own row (smem, odd pitch: conflict-free across the
+// warp's rows), so a CTA's ~110 tokens decide in parallel instead of ~10 per warp in sequence.
+// Returns 1: routed (picks in *p0/*p1, max logit in *zmax; the softmax is written by route_softmax);
+// 0: candidates appended to the pair list; 2: needs the full exact pass.
+__device__ int route_decide_thread(const LaunchParams& P, const float* row, int tok, int t, const GateSmem& g,
+                                   const float* __restrict__ sWn, int* s_np, int* p0o, int* p1o, float* zmax) {
+    const int E = P.E, K = P.k;
+    const float na = __double2float_ru(sqrt(g.sNa[t] * (1.0 + 1e-5)));
+    const float c_s = P.gate_u * 64.0f * g.sSab[t];
+    const float c_w = P.gate_u * P.gate_k1_tc * na;
+    // pass 1: overflow guard, max z~, the k largest lower bounds
+    float z0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY;
+    bool bad = false;
+#pragma unroll 8
+    for (int e = 0; e < E; ++e) {   // branch-free (divergent branches cost a reconvergence per element)
+        const float z = row[e], bt = c_s + c_w * sWn[e] + 1e-30f;
+        bad |= !(fabsf(z) < 1e30f) || !(bt < 1e30f);
+        z0 = fmaxf(z0, z);
+        const float lb = z - bt;
+        m2 = fmaxf(m2, fminf(m1, lb));   // multiset top-2 of the lower bounds
+        m1 = fmaxf(m1, lb);
+    }
+    if (bad) return 2;   // NaN / inf / overflow: the exact path decides
+    const float Lk = K == 1 ? m1 : m2;
+    // pass 2: candidates (upper bound reaches the k-th lower bound) and their top-k by z~ (ties -> lower id)
+    int n_c = 0, p0 = -1, p1 = -1;
+    float v0 = -INFINITY, v1 = -INFINITY;
+#pragma unroll 8
+    for (int e = 0; e < E; ++e) {
+        const float z = row[e], bt = c_s + c_w * sWn[e] + 1e-30f, ub = z + bt;
+        const bool c = ub >= Lk - gate_margin(ub, Lk, z0);
+        const bool g0 = c && z > v0, g1 = c && !g0 && z > v1;   // strict: ties keep the lower id
+        n_c += c ? 1 : 0;
+        v1 = g0 ? v0 : (g1 ? z : v1);
+        p1 = g0 ? p0 : (g1 ? e : p1);
+        v0 = g0 ? z : v0;
+        p0 = g0 ? e : p0;
+    }
+    if (n_c > kGateMaxCand) return 2;
+    if (n_c == K) {
+        const float b0 = c_s + c_w * sWn[p0] + 1e-30f;
+        float last_lb = v0 - b0;
+        bool ok = true;
+        if (K == 2) {
+            const float b1 = c_s + c_w * sWn[p1] + 1e-30f;
+            ok = last_lb > v1 + b1 + gate_margin(last_lb, v1 + b1, z0);
+            last_lb = v1 - b1;
+        }
+        ok &= last_lb - z0 > -80.0f;   // picks far below the max could tie at zero probability
+        if (ok) {
+            *p0o = p0;
+            *p1o = p1;
+            *zmax = z0;
+            return 1;
+        }
+    }
+    // the candidates (ascending expert id) become (token, expert) pairs for the exact pair pass (slots past
+    // the list's capacity are dropped and the token goes to the full pass; every slot below it is filled)
+    const int base = atomicAdd(s_np, n_c);
+    int pos = base;
+    for (int e = 0; e < E; ++e) {
+        const float z = row[e], bt = c_s + c_w * sWn[e] + 1e-30f, ub = z + bt;
+        if (ub >= Lk - gate_margin(ub, Lk, z0)) {
+            if (pos < kGatePairCap) { g.sPT[pos] = tok; g.sPE[pos] = e; }
+            ++pos;
+        }
+    }
+    if (pos > kGatePairCap) return 2;
+    g.sTP0[t] = base;
+    g.sTNC[t] = n_c;
+    return 0;
+}
+
+// Softmax and routing outputs of the thread-decided tokens of a sub-tile (whole CTA): exps over the flat
+// (token, expert) range by every thread, then one warp per token sums, normalises and writes G_phi
+// (coalesced) and the picks -- write_routing_from_row's outputs (G_phi / weights from z~: tolerance).
+__device__ void route_softmax(const LaunchParams& P, const RankCtx& R, const GateSmem& g, int Lp, int tok0, int ts,
+                              const int* sDec, const float* sZ0, int cta) {
+    const int E = P.E, K = P.k, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < ts * E; i += kThreads) {
+        const int t = i / E, e = i - t * E;
+        if (sDec[t] < 0) continue;
+        float* x = g.sL + t * Lp + e;
+        // G_phi / weights of certified tokens carry z~'s tolerance anyway: CUDA's FP32 expf (<= 2 ulp, no
+        // FP64) instead of the bit-exact glibc restatement the exact paths use
+        *x = expf(__fsub_rn(*x, sZ0[t]));
+    }
+    __syncthreads();
+    if (tid == 0) R.trace[(size_t)cta * kTracePts + kTrGateExp] = globaltimer();
+    for (int t = warp; t < ts; t += kThreads / 32) {
+        const int d = sDec[t];
+        if (d < 0) continue;
+        const float* row = g.sL + t * Lp;
+        float part = 0.0f;
+        for (int e = lane; e < E; e += 32) part += row[e];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        const float inv = 1.0f / part;
+        const int tok = tok0 + t;
+        for (int e = lane; e < E; e += 32) R.g_phi[(size_t)tok * E + e] = row[e] * inv;
+        if (lane == 0) {
+            const int p0 = d & 0xffff, p1 = d >> 16;
+            const float q0 = row[p0] * inv, q1 = K == 2 ? row[p1] * inv : 0.0f;
+            const float denom = q0 + q1;
+            R.pick_e[(size_t)tok * K] = p0;
+            R.pick_w[(size_t)tok * K] = denom > 0.0f ? q0 / denom : 0.0f;
+            atomicAdd(&g.sCnt[p0], 1);
+            if (K == 2) {
+                R.pick_e[(size_t)tok * K + 1] = p1;
+                R.pick_w[(size_t)tok * K + 1] = denom > 0.0f ? q1 / denom : 0.0f;
+                atomicAdd(&g.sCnt[p1], 1);
+            }
+        }
+    }
 }
 
 // Exact reference logits of np (token, expert) pairs: thread p runs pair p's separately-rounded
@@ -750,7 +872,7 @@ __device__ void gate_pairs_exact(const LaunchParams& P, const RankCtx& R, const 
 __device__ void gate_full_exact(const LaunchParams& P, const RankCtx& R, const float* __restrict__ A,
                                 const GateSmem& g, int nf) {
     const int E = P.E, H = P.H, Ep = (E + 7) & ~7, tid = threadIdx.x;
-    const int cap = kGateRegionFloats - g.sub * Ep;   // floats after sL (the cp.async staging area)
+    const int cap = kGateRegionFloats - (int)(g.sA - g.sL);   // floats after sL (the cp.async staging area)
     int X = (cap / (2 * (Ep + 1))) & ~31;
     X = X < 32 ? 32 : (X > 256 ? 256 : X);
     float* buf = g.sA;   // [2][X][Ep] Wg rows, then [2][X] token values
@@ -835,23 +957,28 @@ __device__ bool route_resolve(const LaunchParams& P, const RankCtx& R, float* ro
     // exact logits of the candidates replace z~ (G_phi / weights from the row: tolerance)
     if (lane < n_c) row[ec] = zc;
     __syncwarp();
-    write_routing_from_row(P, R, row, m, tok, pe, g.sCnt);
+    write_routing_from_row(P, R, row, m, tok, pe, g.sCnt, g.tab);
     return true;
 }
 
 __device__ void gate_phase(const LaunchParams& P, const RankCtx& R, const float* __restrict__ A, int cta,
-                           uint8_t* smem, unsigned long long* stat) {
+                           uint8_t* smem, unsigned long long* stat, const unsigned long long* tab) {
     const int E = P.E;
     const int Ep = (E + 7) & ~7;
     const int tid = threadIdx.x, warp = tid >> 5;
     constexpr int kWarps = kThreads / 32;
     GateSmem g;
     g.sub = gate_sub(Ep);
+    g.tab = tab;
+    // thread-per-token certified routing (tensor-core logits): rows at an odd pitch (conflict-free)
+    const bool thread_route = P.gate_tc && !P.exact_gate && P.k <= 2 && E <= 128;
+    const int Lp = thread_route ? Ep + 1 : Ep;
     float* region = reinterpret_cast<float*>(smem);
     g.sL = region;
-    g.sA = g.sL + g.sub * Ep;
+    g.sA = g.sL + g.sub * Lp;
     g.sW = g.sA + kGateStages * g.sub * kGateApitch;
-    g.sPair = g.sL + kGateSubMax * 128 > g.sL + g.sub * Ep ? g.sL + kGateSubMax * 128 : g.sL + g.sub * Ep;
+    g.sPair = g.sL + kGateSubMax * 129 > g.sL + g.sub * Lp ? g.sL + kGateSubMax * 129 : g.sL + g.sub * Lp;
+    float* sWn = g.sW;   // thread route: |w_e| (the SIMT staging area is unused with tensor-core logits)
     uint8_t* tail = smem + ((kGateRegionFloats * 4 + 15) & ~15);
     g.sNa = reinterpret_cast<double*>(tail);                    tail += kGateSubMax * 8;
     g.sCnt = reinterpret_cast<int*>(tail);                      tail += kMaxExperts * 4;
@@ -883,7 +1010,7 @@ __device__ void gate_phase(const LaunchParams& P, const RankCtx& R, const float*
         if (P.exact_gate) {
             if (small) gate_logits<false, 1, 4>(P, R, A, tokA + s0, nullptr, ts, g);
             else gate_logits<false, kGateTT, kGateTE>(P, R, A, tokA + s0, nullptr, ts, g);
-            for (int t = warp; t < ts; t += kWarps) route_exact(P, R, g.sL + t * Ep, tokA + s0 + t, g.sCnt);
+            for (int t = warp; t < ts; t += kWarps) route_exact(P, R, g.sL + t * Ep, tokA + s0 + t, g.sCnt, g.tab);
             n_full += ts;
             continue;
         }
@@ -891,39 +1018,80 @@ __device__ void gate_phase(const LaunchParams& P, const RankCtx& R, const float*
         if (tid == 0) { s_np = 0; s_nfull = 0; }
         __syncthreads();
         if (P.gate_tc) {   // tensor-core logits (phase 1a) and row norms from global
-            for (int i = tid; i < ts * Ep; i += kThreads) {
-                const int t = i / Ep, e = i - t * Ep;
-                g.sL[i] = e < E ? R.g_phi[(size_t)(tokA + s0 + t) * E + e] : 0.0f;
+            if ((E & 3) == 0) {   // float4 rows, every load of a thread in flight before its stores
+                const int q4 = E >> 2, n4 = ts * q4;
+                const float4* src = reinterpret_cast<const float4*>(R.g_phi + (size_t)(tokA + s0) * E);
+                for (int i0 = tid; i0 < n4; i0 += kThreads * 8) {
+                    float4 v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        if (i0 + u * kThreads < n4) v[u] = __ldcg(src + i0 + u * kThreads);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int i = i0 + u * kThreads;
+                        if (i < n4) {
+                            float* d = g.sL + (i / q4) * Lp + 4 * (i % q4);
+                            d[0] = v[u].x; d[1] = v[u].y; d[2] = v[u].z; d[3] = v[u].w;
+                        }
+                    }
+                }
+                for (int i = tid; i < ts * (Ep - E); i += kThreads)
+                    g.sL[(i / (Ep - E)) * Lp + E + i % (Ep - E)] = 0.0f;
+            } else {
+                for (int i = tid; i < ts * Ep; i += kThreads) {
+                    const int t = i / Ep, e = i - t * Ep;
+                    g.sL[t * Lp + e] = e < E ? R.g_phi[(size_t)(tokA + s0 + t) * E + e] : 0.0f;
+                }
             }
             for (int t = tid; t < ts; t += kThreads) {
                 g.sNa[t] = R.gate_na[tokA + s0 + t];
                 g.sSab[t] = R.gate_sab[tokA + s0 + t];
             }
+            if (thread_route)
+                for (int e = tid; e < E; e += kThreads) sWn[e] = R.wg_norm[e];
             __syncthreads();
         } else if (small) gate_logits<true, 1, 4>(P, R, A, tokA + s0, nullptr, ts, g);
         else gate_logits<true, kGateTT, kGateTE>(P, R, A, tokA + s0, nullptr, ts, g);
-        for (int t = warp; t < ts; t += kWarps) {
-            const int r = route_certified(P, R, g.sL + t * Ep, tokA + s0 + t, t, g, &s_np);
-            if (r == 2 && (tid & 31) == 0) g.sFull[atomicAdd(&s_nfull, 1)] = tokA + s0 + t;
+        if (tid == 0) R.trace[(size_t)cta * kTracePts + kTrGateLoad] = globaltimer();
+        if (thread_route) {
+            // decisions (thread per token), then the softmax / outputs of the routed ones (whole CTA)
+            int* sDec = reinterpret_cast<int*>(sWn + E);   // (p1 << 16 | p0), -1: not routed here
+            float* sZ0 = reinterpret_cast<float*>(sDec + kGateSubMax);
+            for (int t = tid; t < ts; t += kThreads) {
+                int p0 = 0, p1 = 0;
+                float z0 = 0.0f;
+                const int r = route_decide_thread(P, g.sL + t * Lp, tokA + s0 + t, t, g, sWn, &s_np, &p0, &p1, &z0);
+                sDec[t] = r == 1 ? (p0 | ((P.k == 2 ? p1 : 0) << 16)) : -1;
+                sZ0[t] = z0;
+                if (r == 2) g.sFull[atomicAdd(&s_nfull, 1)] = tokA + s0 + t;
+            }
+            __syncthreads();
+            if (tid == 0) R.trace[(size_t)cta * kTracePts + kTrGateDecide] = globaltimer();
+            route_softmax(P, R, g, Lp, tokA + s0, ts, sDec, sZ0, cta);
+        } else {
+            for (int t = warp; t < ts; t += kWarps) {
+                const int r = route_certified(P, R, g.sL + t * Ep, tokA + s0 + t, t, g, &s_np);
+                if (r == 2 && (tid & 31) == 0) g.sFull[atomicAdd(&s_nfull, 1)] = tokA + s0 + t;
+            }
         }
         __syncthreads();
         if (tid == 0) R.trace[(size_t)cta * kTracePts + kTrGateLogits] = globaltimer();
         const int np = min(s_np, kGatePairCap);
-        if (np > 0 && !(P.debug & kDbgGateNoFlush)) {
+        if (np > 0 && !(FD_DBG(kDbgGateNoFlush))) {
             gate_pairs_exact(P, R, A, g, np);
             for (int t = warp; t < ts; t += kWarps) {
                 if (g.sTNC[t] == 0) continue;
                 ++n_pair_tok;
-                if (!route_resolve(P, R, g.sL + t * Ep, tokA + s0 + t, t, g) && (tid & 31) == 0)
+                if (!route_resolve(P, R, g.sL + t * Lp, tokA + s0 + t, t, g) && (tid & 31) == 0)
                     g.sFull[atomicAdd(&s_nfull, 1)] = tokA + s0 + t;
             }
             __syncthreads();
         }
         if (tid == 0) R.trace[(size_t)cta * kTracePts + kTrGatePairs] = globaltimer();
         const int nf = s_nfull;
-        if (nf > 0 && !(P.debug & kDbgGateNoFlush)) {   // ties / near-ties / overflow: the reference chain for all E
+        if (nf > 0 && !(FD_DBG(kDbgGateNoFlush))) {   // ties / near-ties / overflow: the reference chain for all E
             gate_full_exact(P, R, A, g, nf);
-            for (int t = warp; t < nf; t += kWarps) route_exact(P, R, g.sL + t * Ep, g.sFull[t], g.sCnt);
+            for (int t = warp; t < nf; t += kWarps) route_exact(P, R, g.sL + t * Ep, g.sFull[t], g.sCnt, g.tab);
             n_full += nf;
         }
         __syncthreads();
@@ -1311,6 +1479,9 @@ __device__ int resolve_tile_rows(const LaunchParams& P, const RankCtx& R, Task& 
 }
 
 // Wait accounting (device trace slots 8..15): cycles each role spends blocked on a pipeline edge.
+// Compiled in only for profiling builds (-DFDMOE_WAIT_ACCOUNTING, tools/phase_trace.py): two clock reads
+// around every pipeline wait cost the single MMA issuer measurable tensor-pipe bubbles.
+#ifdef FDMOE_WAIT_ACCOUNTING
 #define FD_TIMED_WAIT(acc, expr)              \
     ({                                        \
         const long long _t0 = clk();          \
@@ -1318,6 +1489,17 @@ __device__ int resolve_tile_rows(const LaunchParams& P, const RankCtx& R, Task& 
         acc += clk() - _t0;                   \
         _ok;                                  \
     })
+#else
+#define FD_TIMED_WAIT(acc, expr) (expr)
+#endif
+// clock reads of the role-level profiling counters (trace slots, chunk log): compiled out of the product
+__device__ __forceinline__ long long pclk() {
+#ifdef FDMOE_WAIT_ACCOUNTING
+    return clk();
+#else
+    return 0;
+#endif
+}
 
 // warp 10, one lane: fetch tiles, resolve dependencies, stream both operands
 template <int PREC>
@@ -1343,7 +1525,7 @@ __device__ void gemm_producer(const LaunchParams& P, const RankCtx& R, uint8_t* 
     const uint64_t pol_w = l2_policy_evict_first();
     const uint64_t pol_x = l2_policy_evict_last();
     while (true) {
-        const long long tf0 = clk();
+        const long long tf0 = pclk();
         const uint32_t t = atomicAdd(R.gemm_head, 1u);
         Task tk;
         bool end = t >= n_g0 + n_g1;
@@ -1356,7 +1538,7 @@ __device__ void gemm_producer(const LaunchParams& P, const RankCtx& R, uint8_t* 
                 if (!wait_counter(P, R, R.g0done + (size_t)tk.le * P.MT + tk.m, (uint32_t)P.NB0, 302)) end = true;
             }
         }
-        t_fetch += clk() - tf0;
+        t_fetch += pclk() - tf0;
         if (!mbar_wait(&G.qempty[q], qphase ^ 1u, P.abort_flag)) end = true;
         if (end) {
             G.ring[q].type = -1;
@@ -1385,7 +1567,7 @@ __device__ void gemm_producer(const LaunchParams& P, const RankCtx& R, uint8_t* 
         for (int kb = 0; kb < nk; ++kb) {
             // weight tile first: the converter warps need it one step before the MMA does
             if (!FD_TIMED_WAIT(w_w, mbar_wait(&G.wempty[wstage], wphase ^ 1u, P.abort_flag))) return;
-            if (P.debug & kDbgNoWTma) mbar_arrive(&G.wfull[wstage]);
+            if (FD_DBG(kDbgNoWTma)) mbar_arrive(&G.wfull[wstage]);
             else {
                 mbar_expect_tx(&G.wfull[wstage], Cfg::W_BYTES);
 #pragma unroll
@@ -1397,7 +1579,7 @@ __device__ void gemm_producer(const LaunchParams& P, const RankCtx& R, uint8_t* 
 
             if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.done[stage], phase ^ 1u, P.abort_flag))) return;
             uint8_t* st = ring + stage * Cfg::STAGE_BYTES;
-            if (P.debug & kDbgNoXTma) mbar_arrive(&G.ready[stage]);
+            if (FD_DBG(kDbgNoXTma)) mbar_arrive(&G.ready[stage]);
             else {
                 mbar_expect_tx(&G.ready[stage], Cfg::STAGE_BYTES);
 #pragma unroll
@@ -1448,9 +1630,9 @@ __device__ void gemm_wconvert(const LaunchParams& P, uint8_t* ring, GemmCtrl& G,
         const int nk = (task_k(P, type) + Cfg::BK - 1) / Cfg::BK;
         double ss = 0.0;   // gate tile: sum of squares of this row (float per stage, double across stages)
         for (int kb = 0; kb < nk; ++kb) {
-            const long long c0 = clk();
+            const long long c0 = pclk();
             if (!FD_TIMED_WAIT(w_w, mbar_wait(&G.wfull[wst], wphase, P.abort_flag))) return;
-            const long long c1 = clk();
+            const long long c1 = pclk();
             const uint8_t* wrow = ring + Cfg::W_OFF + wst * Cfg::W_BYTES + r * 128;
             float4 c[Cfg::NATOM][8];
 #pragma unroll
@@ -1467,8 +1649,8 @@ __device__ void gemm_wconvert(const LaunchParams& P, uint8_t* ring, GemmCtrl& G,
             if (lane == 0) mbar_arrive(&G.wempty[wst]);   // values are in registers: slot reusable
             if (++wst == Cfg::WSTAGES) { wst = 0; wphase ^= 1u; }
 
-            const long long c2 = clk();
-            if (PREC == kFP32 && g_norm) {
+            const long long c2 = pclk();
+            if (PREC == kFP32 && g_norm && !FD_DBG(kDbgGateNoNorm)) {
                 float cs = 0.0f;
 #pragma unroll
                 for (int at = 0; at < Cfg::NATOM; ++at)
@@ -1491,6 +1673,7 @@ __device__ void gemm_wconvert(const LaunchParams& P, uint8_t* ring, GemmCtrl& G,
                     const uint32_t col = tmem + lane_addr + Cfg::TMEM_A0 + ast * Cfg::A_COLS;
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {   // 16 K values per half atom
+                        if (FD_DBG(kDbgNoConvert)) break;
                         uint32_t hi[16], lo[16];
 #pragma unroll
                         for (int i = 0; i < 4; ++i) {
@@ -1515,10 +1698,10 @@ __device__ void gemm_wconvert(const LaunchParams& P, uint8_t* ring, GemmCtrl& G,
                 continue;
             }
             if (!FD_TIMED_WAIT(w_a, mbar_wait(&G.done[ast], aphase ^ 1u, P.abort_flag))) return;
-            const long long c3 = clk();
+            const long long c3 = pclk();
             tc_fence_after();
             const uint32_t col = tmem + lane_addr + Cfg::TMEM_A0 + ast * Cfg::A_COLS;
-            if (P.debug & kDbgNoConvert) {
+            if (FD_DBG(kDbgNoConvert)) {
             } else {
 #pragma unroll
                 for (int at = 0; at < Cfg::NATOM; ++at)
@@ -1541,7 +1724,7 @@ __device__ void gemm_wconvert(const LaunchParams& P, uint8_t* ring, GemmCtrl& G,
             if (clog && lane == 0 && nlog < kChunkLog / 2) {
                 // chunklog rows [256, 512): converter warp 0 per stage: wfull wait, LDS, done wait, convert+st
                 unsigned long long* o = clog + 4 * (kChunkLog / 2 + nlog++);
-                o[0] = c1 - c0; o[1] = c2 - c1; o[2] = c3 - c2; o[3] = clk() - c3;
+                o[0] = c1 - c0; o[1] = c2 - c1; o[2] = c3 - c2; o[3] = pclk() - c3;
             }
             if (++ast == Cfg::STAGES) { ast = 0; aphase ^= 1u; }
         }
@@ -1614,6 +1797,7 @@ __device__ __forceinline__ void issue_half_fp32(uint32_t d_main, uint32_t d_corr
     }
 }
 
+constexpr int kCorrInMainMax = 2;
 struct MmaFp32State {
     int stage = 0, ah = 0;
     uint32_t phase = 0, ahph = 0, cph = 0;
@@ -1628,6 +1812,17 @@ __device__ __forceinline__ bool mma_tile_fp32(const LaunchParams& P, uint8_t* ri
                                               long long& w_x) {
     using Cfg = GemmCfg<kFP32>;
     const uint32_t d_corr = tmem + kTmemCorr;
+    // The correction accumulator is free once the epilogue folded the previous tile's corrections
+    // (cempty). Until then -- for at most kCorrInMainMax half-stages -- the correction products go into the
+    // main accumulator (<= 16 extra truncating MMAs at the start of the sum, where the partial sums are
+    // smallest) instead of stalling the tensor pipe; after that the issuer blocks on the fold. The first
+    // correction product after the fold starts kTmemCorr fresh. (Unbounded, the main accumulator took
+    // every correction of a tile whenever the epilogue ran a tile behind: worst element 1.17x the FP32
+    // bound at c4 EP8 -- tests/test_gpu_baseline.py.)
+    bool corr_free = false;
+    const int nhalf = nk * Cfg::NATOM;
+    // (Probing the next half-stage's barriers between this half-stage's MMAs, so the boundary skips its
+    // wait, measured slower: 1.581 -> 1.606 ms at c4. The single issuer keeps plain waits.)
     for (int kb = 0; kb < nk; ++kb) {
         if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.ready[st.stage], st.phase, P.abort_flag))) return false;
         tc_fence_after();
@@ -1638,14 +1833,24 @@ __device__ __forceinline__ bool mma_tile_fp32(const LaunchParams& P, uint8_t* ri
             tc_fence_after();
             const uint32_t a_half = tmem + Cfg::TMEM_A0 + st.ah * Cfg::A_COLS;
             const uint64_t bd = bdesc + ((at * Cfg::ATOM_BYTES) >> 4);
-            if (kb == 0 && at == 0) {
-                issue_half_fp32<true, false>(d_main, d_corr, a_half, bd, idesc, 0u, 0u);
-                if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.cempty, st.cph ^ 1u, P.abort_flag))) return false;
-                st.cph ^= 1u;
-                tc_fence_after();
-                issue_half_fp32<false, true>(d_main, d_corr, a_half, bd, idesc, 0u, 0u);
+            const bool first = kb == 0 && at == 0;
+            if (corr_free) {
+                issue_half_fp32<true, true>(d_main, d_corr, a_half, bd, idesc, first ? 0u : 1u, 1u);
             } else {
-                issue_half_fp32<true, true>(d_main, d_corr, a_half, bd, idesc, 1u, 1u);
+                issue_half_fp32<true, false>(d_main, d_corr, a_half, bd, idesc, first ? 0u : 1u, 0u);
+                const int h = kb * Cfg::NATOM + at;
+                corr_free = mbar_test_wait(&G.cempty, st.cph ^ 1u);
+                if (!corr_free && (h + 1 >= kCorrInMainMax || h + 1 == nhalf)) {
+                    if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.cempty, st.cph ^ 1u, P.abort_flag))) return false;
+                    corr_free = true;
+                }
+                if (corr_free) {
+                    st.cph ^= 1u;
+                    tc_fence_after();
+                    issue_half_fp32<false, true>(d_main, d_corr, a_half, bd, idesc, 0u, 0u);
+                } else {   // corrections of this half-stage ride in the main accumulator
+                    issue_half_fp32<false, true>(d_main, d_main, a_half, bd, idesc, 0u, 1u);
+                }
             }
             mma_commit(&G.aempty[st.ah]);
             if (++st.ah == Cfg::A_SLOTS) { st.ah = 0; st.ahph ^= 1u; }
@@ -1746,7 +1951,7 @@ __device__ void gemm_mma(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, unsi
             if (++acc == kAccStages) { acc = 0; accphase ^= 1u; }
             continue;
         }
-        long long t_rdy = chunklog ? clk() : 0;
+        long long t_rdy = chunklog ? pclk() : 0;
         if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.ready[stage], phase, P.abort_flag))) return;
         tc_fence_after();
         if (Cfg::STAGES == 2 && stage == 0 && (nk & 1) == 0 && !chunklog) {
@@ -1776,7 +1981,7 @@ __device__ void gemm_mma(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, unsi
         }
 #pragma unroll 4   // fewer loop back-edges (and their YIELDs) between stages (measured: 4 beats 1/2/8/16)
         for (int kb = 0; kb < nk; ++kb) {
-            const long long t_iss = chunklog ? clk() : 0;
+            const long long t_iss = chunklog ? pclk() : 0;
             const uint32_t abase = tmem + Cfg::TMEM_A0 + stage * Cfg::A_COLS;
             const uint64_t bdesc = umma_desc_kmajor(smem_u32(ring + stage * Cfg::STAGE_BYTES), 128);
             const int nstage = stage + 1 == Cfg::STAGES ? 0 : stage + 1;
@@ -1791,7 +1996,7 @@ __device__ void gemm_mma(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, unsi
             issue_stage<PREC, kProbeAt, NM>(d_tmem, abase, bdesc, kb == 0);
             mma_commit(&G.done[stage]);   // token + weight stage reusable once these MMAs retire
             if (chunklog && nlog < kChunkLog / 2) {
-                chunklog[4 * nlog] = clk();
+                chunklog[4 * nlog] = pclk();
                 chunklog[4 * nlog + 1] = t_rdy;   // wait for ready started (bit 62: ready already)
                 chunklog[4 * nlog + 2] = t_iss;   // ready observed, issue starts
                 chunklog[4 * nlog + 3] = 0;
@@ -1800,7 +2005,7 @@ __device__ void gemm_mma(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, unsi
             stage = nstage;
             phase = nphase;
             if (!last) {
-                if (chunklog) t_rdy = clk() | ((long long)nrdy << 62);
+                if (chunklog) t_rdy = pclk() | ((long long)nrdy << 62);
                 if (!nrdy && !FD_TIMED_WAIT(w_x, mbar_wait(&G.ready[stage], phase, P.abort_flag))) return;
                 tc_fence_after();
             }
@@ -1953,7 +2158,7 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
                 if (!wait_counter(P, R, P.ranks[r].zero_ctr, P.zero_target, 310)) return;
             zero_seen = true;
         }
-        const long long tb0 = clk();
+        const long long tb0 = pclk();
         long long e_loop = 0, e_bar = 0, e_ld = 0;
 
         const int ncols = type == 0 ? P.D : P.H;
@@ -1997,7 +2202,14 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
 #pragma unroll 1
         for (int ch = 0; ch < kNT / 32; ++ch) {
             uint32_t r[32];
-            const long long tl0 = clk();
+            // this chunk's row pointer / weight by register selects (indexing the arrays with the runtime
+            // ch would put them in local memory: two LDL per row in the store loop)
+            float* rowp_c = rowp[0];
+            float roww_c = roww[0];
+#pragma unroll
+            for (int c = 1; c < kNT / 32; ++c)
+                if (ch == c) { rowp_c = rowp[c]; roww_c = roww[c]; }
+            const long long tl0 = pclk();
             tmem_ld32(tbase + ch * 32, r);
             // validity of the 32 token rows of this chunk: bit i = row ch*32+i holds a landed token
             uint32_t vmask;
@@ -2013,8 +2225,8 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
                 }
             }
             tmem_wait_ld();
-            e_ld += clk() - tl0;
-            if (!fvalid || (P.debug & kDbgNoEpiStore)) vmask = 0;
+            e_ld += pclk() - tl0;
+            if (!fvalid || (FD_DBG(kDbgNoEpiStore))) vmask = 0;
             // separate compact loops per tile type and activation (one fully unrolled body with every
             // variant inlined — erff included — was ~20 KB of SASS streamed through the I-cache per chunk)
             if (type == 0) {
@@ -2031,11 +2243,11 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
                     const float v = __fadd_rn(__uint_as_float(r[i]), bias);
                     // row n's pointer (and weight) from lane i of this chunk's prefetch
                     float* rp = reinterpret_cast<float*>(
-                        __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(rowp[ch]), i));
+                        __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(rowp_c), i));
                     if (FUSED) {
                         // combine fused here (oracle.hpp:102-107 with k <= 2): O[t] += fl(w * y); the
                         // origin's slot table gives the token and its combine weight
-                        const float w = __shfl_sync(0xffffffffu, roww[ch], i);
+                        const float w = __shfl_sync(0xffffffffu, roww_c, i);
                         atomicAdd(rp + feat, __fmul_rn(w, v));
                     } else {
                         rp[feat] = v;
@@ -2043,10 +2255,10 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
                 }
             }
         }
-        e_loop = clk();
+        e_loop = pclk();
         tc_fence_before();
         asm volatile("bar.sync 1, 128;" ::: "memory");   // all rows stored, TMEM drained
-        e_bar = clk();
+        e_bar = pclk();
         if (et == 0) {
             mbar_arrive(&G.tempty[acc]);
             // the tile's release signals (fence + counters / flags) go to the signal warp: the epilogue
@@ -2057,10 +2269,10 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
             if (++sq == kTaskRing) { sq = 0; sphase ^= 1u; }
             mbar_arrive(&G.qempty[q]);
         }
-        busy += clk() - tb0;
+        busy += pclk() - tb0;
         if (elog && et == 0 && nelog < kChunkLog / 2) {   // chunklog rows [256, 512): per tile
             unsigned long long* o = elog + 4 * (kChunkLog / 2 + nelog++);
-            o[0] = type; o[1] = e_loop - tb0; o[2] = e_ld; o[3] = clk() - e_bar;
+            o[0] = type; o[1] = e_loop - tb0; o[2] = e_ld; o[3] = pclk() - e_bar;
         }
         if (++q == kTaskRing) { q = 0; qphase ^= 1u; }
         if (++acc == kAccStages) { acc = 0; accphase ^= 1u; }
@@ -2099,21 +2311,27 @@ __device__ void gate_producer(const LaunchParams& P, const RankCtx& R, int rl, u
             if (++q == kTaskRing) { q = 0; qphase ^= 1u; }
             for (int kb = 0; kb < nk; ++kb) {
                 if (!mbar_wait(&G.wempty[wstage], wphase ^ 1u, P.abort_flag)) return;
-                mbar_expect_tx(&G.wfull[wstage], Cfg::W_BYTES);
+                if (FD_DBG(kDbgGateNoTokTma)) mbar_arrive(&G.wfull[wstage]);
+                else {
+                    mbar_expect_tx(&G.wfull[wstage], Cfg::W_BYTES);
 #pragma unroll
-                for (int at = 0; at < Cfg::NATOM; ++at)
-                    tma_load_2d_hint(ring + Cfg::W_OFF + wstage * Cfg::W_BYTES + at * Cfg::ATOM_BYTES, ta,
-                                     &G.wfull[wstage], kb * Cfg::BK + at * Cfg::ATOM_K, tok0, pol);
+                    for (int at = 0; at < Cfg::NATOM; ++at)
+                        tma_load_2d_hint(ring + Cfg::W_OFF + wstage * Cfg::W_BYTES + at * Cfg::ATOM_BYTES, ta,
+                                         &G.wfull[wstage], kb * Cfg::BK + at * Cfg::ATOM_K, tok0, pol);
+                }
                 if (++wstage == Cfg::WSTAGES) { wstage = 0; wphase ^= 1u; }
                 if (!mbar_wait(&G.done[stage], phase ^ 1u, P.abort_flag)) return;
                 uint8_t* st = ring + stage * Cfg::STAGE_BYTES;
-                mbar_expect_tx(&G.ready[stage], bbytes);
+                if (FD_DBG(kDbgGateNoWgTma)) mbar_arrive(&G.ready[stage]);
+                else {
+                    mbar_expect_tx(&G.ready[stage], bbytes);
 #pragma unroll
-                for (int pl = 0; pl < Cfg::PLANES; ++pl)
+                    for (int pl = 0; pl < Cfg::PLANES; ++pl)
 #pragma unroll
-                    for (int at = 0; at < Cfg::NATOM; ++at)
-                        tma_load_2d_hint(st + pl * Cfg::PLANE_BYTES + at * Cfg::ATOM_BYTES, &R.tm_wg[pl], &G.ready[stage],
-                                         kb * Cfg::BK + at * Cfg::ATOM_K, eb * P.gate_n, pol);
+                        for (int at = 0; at < Cfg::NATOM; ++at)
+                            tma_load_2d_hint(st + pl * Cfg::PLANE_BYTES + at * Cfg::ATOM_BYTES, &R.tm_wg[pl],
+                                             &G.ready[stage], kb * Cfg::BK + at * Cfg::ATOM_K, eb * P.gate_n, pol);
+                }
                 if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
             }
         }
@@ -2149,20 +2367,24 @@ __device__ void gate_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
             if (!mbar_wait(&G.tfull[acc], accphase, P.abort_flag)) return;
             tc_fence_after();
             float m = 0.0f;
+            if (FD_DBG(kDbgGateNoEpi)) goto folded;
+            // 32-column chunks: one TMEM load round trip per 32 columns (the fold is on the gate's
+            // critical path: the MMA warp reuses this accumulator two stages later)
 #pragma unroll
-            for (int ch = 0; ch < kBF / 16; ++ch) {
-                if (ch * 16 < P.gate_n) {
-                    uint32_t v[16];
-                    tmem_ld16(tmem + lanes + (uint32_t)(acc * kNT + ch * 16), v);
+            for (int ch = 0; ch < kBF / 32; ++ch) {
+                if (ch * 32 < P.gate_n) {
+                    uint32_t v[32];
+                    tmem_ld32(tmem + lanes + (uint32_t)(acc * kNT + ch * 32), v);
                     tmem_wait_ld();
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        z[ch * 16 + i] = __fadd_rn(z[ch * 16 + i], __uint_as_float(v[i]));
-                        if (ch * 16 + i < nv) m = fmaxf(m, fabsf(z[ch * 16 + i]));
+                    for (int i = 0; i < 32; ++i) {
+                        z[ch * 32 + i] = __fadd_rn(z[ch * 32 + i], __uint_as_float(v[i]));
+                        if (ch * 32 + i < nv) m = fmaxf(m, fabsf(z[ch * 32 + i]));
                     }
                 }
             }
             sab = __fadd_ru(sab, m);
+        folded:
             tc_fence_before();
             __syncwarp();
             if ((et & 31) == 0) mbar_arrive(&G.tempty[acc]);
@@ -2329,7 +2551,9 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
     const int tid = threadIdx.x, warp = tid >> 5;
     __shared__ unsigned long long s_stat[5];   // gemm0/gemm1 tiles, combine tasks, full-exact / pair-resolved gate tokens
     __shared__ int s_n_expert[kMaxExperts];   // kept rows per expert of this rank (dispatch -> combine)
+    __shared__ unsigned long long s_exp_tab[32];   // glibc expf table (divergent lookups: smem, not __constant__)
     if (tid < 5) s_stat[tid] = 0;
+    if (tid < 32) s_exp_tab[tid] = c_exp_tab[tid];
     unsigned long long* trace = R.trace + (size_t)cta * kTracePts;
     if (tid == 0) trace[0] = globaltimer();
 
@@ -2377,7 +2601,7 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
         if (tid == 0) trace[kTrGateTc] = globaltimer();
     }
     // phase 1b: routing (certified from the tensor-core logits, or the SIMT gate), smem region as scratch
-    gate_phase(P, R, A, cta, smem, s_stat);
+    gate_phase(P, R, A, cta, smem, s_stat, s_exp_tab);
     if (tid == 0) {
         trace[1] = globaltimer();
         emit_event(P, R, kEvGateDone, cta, 0, trace[0], trace[1], R.rank, -1, -1, -1, -1, 0);
@@ -2484,10 +2708,14 @@ __global__ void prep_transpose_kernel(const float* __restrict__ W, int El, int R
     }
 }
 
+#ifdef FDMOE_DEV   // diagnostics: libfdmoe_dev.so only (include/fdmoe_dev.h)
 // ================================================================ debug entry points
 __global__ void debug_expf_kernel(const float* x, float* y, long long n) {
+    __shared__ unsigned long long s_tab[32];
+    if (threadIdx.x < 32) s_tab[threadIdx.x] = c_exp_tab[threadIdx.x];
+    __syncthreads();
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-        y[i] = expf_glibc(x[i]);
+        y[i] = expf_glibc(x[i], s_tab);
 }
 
 // One tile through the layer's exact machinery (weight loader -> TMEM, TMA token ring,
@@ -2842,6 +3070,8 @@ cudaError_t launch_debug_mma_rate(int kind, int N, int iters, int nissuers, unsi
     return cudaGetLastError();
 }
 
+#endif  // FDMOE_DEV
+
 // ---------------------------------------------------------------- host-visible launchers
 int layer_smem_bytes(int prec) {
     return prec == kFP32 ? SmemPlan<kFP32>::TOTAL : SmemPlan<kBF16>::TOTAL;
@@ -2877,6 +3107,7 @@ cudaError_t launch_prep_transpose(const float* W, int El, int Rr, int Cc, void* 
     return cudaGetLastError();
 }
 
+#ifdef FDMOE_DEV
 cudaError_t launch_debug_expf(const float* x, float* y, long long n, cudaStream_t s) {
     debug_expf_kernel<<<1024, 256, 0, s>>>(x, y, n);
     return cudaGetLastError();
@@ -2894,5 +3125,7 @@ cudaError_t launch_debug_gemm(int prec, const CUtensorMap* t, int K, float* D, u
     }
     return cudaGetLastError();
 }
+
+#endif  // FDMOE_DEV
 
 }  // namespace fdmoe

@@ -289,7 +289,11 @@ fdmoe_status build_ctx(fdmoe_handle* h) {
             c.cnt_cta = r.cnt_cta; c.tbl_tok = r.tbl_tok; c.tbl_w = r.tbl_w; c.slot_counts = r.slot_counts;
             c.blk_ready = r.blk_ready;
             c.trace = r.trace;
+#ifdef FDMOE_DEV
             c.chunklog = getenv("FDMOE_CHUNKLOG") ? r.chunklog : nullptr;
+#else
+            c.chunklog = nullptr;
+#endif
             c.delay_ns = r.delay_ns;
             c.ev = r.ev;
             c.ev_cap = r.ev_cap;
@@ -636,8 +640,12 @@ static fdmoe_status launch_all(fdmoe_handle* h, const float* const* in_dev, floa
                     if (ts) return ts;
                 }
         }
-        const char* dbg = getenv("FDMOE_DEBUG");   // ablation switches (tools/ablate.py); unset in production
+#ifdef FDMOE_DEV
+        const char* dbg = getenv("FDMOE_DEBUG");   // ablation switches (tools/ablate.py): development library only
         p.debug = dbg ? atoi(dbg) : 0;
+#else
+        p.debug = 0;
+#endif
         CK(cudaSetDevice(g.dev));
         cudaStream_t s = g.stream;
         if (streams && streams[g.members[0]]) s = static_cast<cudaStream_t>(streams[g.members[0]]);
@@ -883,14 +891,6 @@ fdmoe_status fdmoe_read_events(fdmoe_handle* h, int32_t local_rank, fdmoe_event*
     return FDMOE_OK;
 }
 
-fdmoe_status fdmoe_read_chunklog(fdmoe_handle* h, uint64_t* out) {
-    RankRes& r = h->ranks[0];
-    CK(cudaSetDevice(r.dev));
-    for (auto& g : h->groups) if (g.dev == r.dev) CK(cudaEventSynchronize(g.ev1));
-    CK(cudaMemcpy(out, r.chunklog, (size_t)kChunkLog * 4 * 8, cudaMemcpyDeviceToHost));
-    return FDMOE_OK;
-}
-
 fdmoe_status fdmoe_last_kernel_ms(fdmoe_handle* h, double* ms) {
     if (!h || !ms) return fail(FDMOE_ERR_CONFIG, "null argument");
     double best = 0.0;
@@ -902,6 +902,15 @@ fdmoe_status fdmoe_last_kernel_ms(fdmoe_handle* h, double* ms) {
         best = std::max(best, (double)v);
     }
     *ms = best;
+    return FDMOE_OK;
+}
+
+#ifdef FDMOE_DEV   // diagnostics: libfdmoe_dev.so only (include/fdmoe_dev.h)
+fdmoe_status fdmoe_read_chunklog(fdmoe_handle* h, uint64_t* out) {
+    RankRes& r = h->ranks[0];
+    CK(cudaSetDevice(r.dev));
+    for (auto& g : h->groups) if (g.dev == r.dev) CK(cudaEventSynchronize(g.ev1));
+    CK(cudaMemcpy(out, r.chunklog, (size_t)kChunkLog * 4 * 8, cudaMemcpyDeviceToHost));
     return FDMOE_OK;
 }
 
@@ -1000,5 +1009,7 @@ fdmoe_status fdmoe_debug_latency(int32_t n, uint64_t* out4) {
     cudaFree(d);
     return FDMOE_OK;
 }
+
+#endif  // FDMOE_DEV
 
 }  // extern "C"

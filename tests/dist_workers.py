@@ -30,3 +30,24 @@ def run(rank: int, world: int, port: int, q):
         q.put((rank, res))
     finally:
         dist.destroy_process_group()
+
+
+def run_bulksync(rank: int, world: int, port: int, q):
+    """One rank of the bulk-synchronous baseline (bulksync.py) over gloo: all_to_all_single dispatch and
+    combine between real processes."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2506_04667_b200 as fd
+        from paper_2506_04667_b200.bulksync import BulkSyncMoE
+        cfg = fd.MoeConfig(tokens_per_device=128, embed_dim=64, ffn_dim=96, experts_total=8, devices=world,
+                           topk=2, seed=3)
+        model = fd.make_model(cfg)
+        shard = fd.make_shards(cfg)[rank]
+        m = BulkSyncMoE(cfg, model, rank=rank, world=world, device="cpu")
+        q.put((rank, m.forward(torch.from_numpy(shard)).numpy()))
+    finally:
+        dist.destroy_process_group()

@@ -13,8 +13,8 @@ import paper_2506_04667_b200 as fd
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def declared_symbols():
-    text = open(os.path.join(ROOT, "include", "fdmoe.h")).read()
+def declared_symbols(header="fdmoe.h"):
+    text = open(os.path.join(ROOT, "include", header)).read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
     return sorted(set(re.findall(r"\b(fdmoe_[A-Za-z_0-9]+)\s*\(", text)))
 
@@ -26,6 +26,20 @@ def test_library_exports_every_declared_symbol():
     missing = [s for s in decl if not hasattr(L, s)]
     assert not missing, missing
     assert set(decl) == set(fd.EXPORTED_SYMBOLS)
+
+
+def test_product_library_has_no_diagnostics_and_dev_library_has_them():
+    """The product .so exports exactly fdmoe.h; the fdmoe_dev.h diagnostics and the FDMOE_DEBUG
+    ablation bits live only in libfdmoe_dev.so (tests/tools)."""
+    dev = declared_symbols("fdmoe_dev.h")
+    assert dev and not set(dev) & set(declared_symbols())
+    L = fd.lib()
+    assert not [s for s in dev if hasattr(L, s)]
+    D = fd.dev_lib()
+    assert not [s for s in dev + declared_symbols() if not hasattr(D, s)]
+    import subprocess
+    strings = subprocess.run(["strings", fd._build.LIB], capture_output=True, text=True).stdout
+    assert "FDMOE_DEBUG" not in strings and "FDMOE_CHUNKLOG" not in strings
 
 
 def test_abi_version():

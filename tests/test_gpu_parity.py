@@ -65,7 +65,7 @@ def test_device_expf_matches_glibc():
         np.array([0.0, -0.0, -1e-45, -87.3, -88.0, -88.72, -103.9, -103.97, -104.0, -150.0, -np.inf], np.float32),
     ]).astype(np.float32)
     y = np.empty_like(x)
-    fd._check(fd.lib().fdmoe_debug_expf(fd._ptr(x), fd._ptr(y), x.size))
+    fd.dev_check(fd.dev_lib().fdmoe_debug_expf(fd._ptr(x), fd._ptr(y), x.size))
     want = po.expf_libm(x)
     mism = np.nonzero(y.view(np.uint32) != want.view(np.uint32))[0]
     assert mism.size == 0, f"{mism.size} mismatches, first x={x[mism[:3]]}"
@@ -80,7 +80,7 @@ def test_tcgen05_tile(prec, K):
     W = rng.standard_normal((128, K)).astype(np.float32)
     X = rng.standard_normal((128, K)).astype(np.float32)
     D = np.empty((128, 128), np.float32)
-    fd._check(fd.lib().fdmoe_debug_gemm(prec, K, fd._ptr(W), fd._ptr(X), fd._ptr(D)))
+    fd.dev_check(fd.dev_lib().fdmoe_debug_gemm(prec, K, fd._ptr(W), fd._ptr(X), fd._ptr(D)))
     if prec == fd.Precision.fp32:
         want = W.astype(np.float64) @ X.astype(np.float64).T
         err = np.abs(D - want).max() / np.abs(want).max()

@@ -4,6 +4,7 @@ import numpy as np
 sys.path.insert(0, '.')
 import torch
 import paper_2506_04667_b200 as fd
+fd.select_library(fd._build.DEV_LIB)   # ablation bits / chunk log: development build
 S = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
 E = int(sys.argv[2]) if len(sys.argv) > 2 else 128
 prec = int(sys.argv[3]) if len(sys.argv) > 3 else 0

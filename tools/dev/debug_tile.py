@@ -5,7 +5,7 @@ for K in (64, 256, 512, 1024, 2048):
     rng = np.random.default_rng(K)
     A = rng.standard_normal((128, K)).astype(np.float32); B = rng.standard_normal((256, K)).astype(np.float32)
     D = np.empty((128, 256), np.float32)
-    fd._check(fd.lib().fdmoe_debug_gemm(0, K, fd._ptr(A), fd._ptr(B), fd._ptr(D)))
+    fd.dev_check(fd.dev_lib().fdmoe_debug_gemm(0, K, fd._ptr(A), fd._ptr(B), fd._ptr(D)))
     want = A.astype(np.float64) @ B.astype(np.float64).T
     f32 = (A @ B.T)  # numpy fp32 (pairwise/blocked sum)
     seq = np.zeros((128,256), np.float32)

@@ -4,6 +4,7 @@ import numpy as np
 sys.path.insert(0, '.')
 import torch
 import paper_2506_04667_b200 as fd
+fd.select_library(fd._build.DEV_LIB)   # ablation bits / chunk log: development build
 S = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
 E = int(sys.argv[2]) if len(sys.argv) > 2 else 128
 cfg = fd.MoeConfig(tokens_per_device=S, embed_dim=2048, ffn_dim=2048, experts_total=E, devices=1, topk=2)

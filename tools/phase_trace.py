@@ -3,6 +3,7 @@ import sys, json, numpy as np
 sys.path.insert(0, '.')
 import torch
 import paper_2506_04667_b200 as fd
+fd.select_library(fd._build.DEV_LIB)   # per-role wait accounting is compiled into the development build only
 S, E = int(sys.argv[1]) if len(sys.argv) > 1 else 16384, int(sys.argv[2]) if len(sys.argv) > 2 else 128
 prec = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 cfg = fd.MoeConfig(tokens_per_device=S, embed_dim=2048, ffn_dim=2048, experts_total=E, devices=1, topk=2,
@@ -12,19 +13,20 @@ x = torch.from_numpy(fd.make_shards(cfg)[0]).cuda(); y = torch.empty_like(x)
 st = torch.cuda.Stream(); torch.cuda.set_stream(st)
 for _ in range(4):
     op.forward_device([x.data_ptr()], [y.data_ptr()], [st.cuda_stream]); op.sync()
-t = op.trace(0) / 1e3   # us
+tr = op.trace(0).astype(np.float64)   # ns (phase columns) / raw counters (7..19)
+t = tr / 1e3   # us
 names = ["start", "gate", "barrier", "dispatch", "ffn", "combine", "end"]
 print("kernel ms", op.last_kernel_ms())
 for i, n in enumerate(names):
     print(f"{n:9s} min {t[:, i].min():9.1f}  med {np.median(t[:, i]):9.1f}  max {t[:, i].max():9.1f} us")
-for i, n in ((28, "gate-tc-logits"), (24, "gate-route"), (25, "gate-pairs"), (26, "gate-full"), (20, "prefix"), (21, "slots"), (22, "slot-barrier"), (23, "push")):
+for i, n in ((28, "gate-tc-logits"), (29, "gate-load"), (30, "gate-decide"), (31, "gate-exp"), (24, "gate-route"), (25, "gate-pairs"), (26, "gate-full"), (20, "prefix"), (21, "slots"), (22, "slot-barrier"), (23, "push")):
     print(f"{n:12s} min {t[:, i].min():9.1f}  med {np.median(t[:, i]):9.1f}  max {t[:, i].max():9.1f} us")
 g = t[:, 1]
 worst = int(np.argmax(g))
 print(f"slowest gate CTA {worst}: logits {t[worst, 24]/1:.1f} pairs {t[worst, 25]:.1f} full {t[worst, 26]:.1f} us "
       f"(full-exact tokens {int(round(t[worst, 27] * 1e3))}); median CTA: logits {np.median(t[:, 24]):.1f} "
       f"pairs {np.median(t[:, 25]):.1f} full {np.median(t[:, 26]):.1f}")
-print("ffn tiles per CTA: min", int(t[:, 7].min()), "max", int(t[:, 7].max()), "sum", int(t[:, 7].sum()))
+print("ffn tiles per CTA: min", int(tr[:, 7].min()), "max", int(tr[:, 7].max()), "sum", int(tr[:, 7].sum()))
 ffn_cyc = (t[:, 4] - t[:, 3]).mean() * 1e3 * 1.965   # ns -> cycles at max clock (approx)
 for i, n in enumerate(["mma<-tokens", "mma<-weights", "mma<-acc", "conv<-wTMA", "conv<-tmemA", "prod<-wslot", "prod<-xslot", "epi<-acc"]):
-    print(f"wait {n:14s} mean {t[:, 8 + i].mean() / 1e3:9.1f} kcyc  ({100 * t[:, 8 + i].mean() / ffn_cyc:5.1f}% of FFN phase)")
+    print(f"wait {n:14s} mean {tr[:, 8 + i].mean() / 1e3:9.1f} kcyc  ({100 * tr[:, 8 + i].mean() / ffn_cyc:5.1f}% of FFN phase)")

@@ -5,6 +5,7 @@ import numpy as np
 sys.path.insert(0, '.')
 import torch
 import paper_2506_04667_b200 as fd
+fd.select_library(fd._build.DEV_LIB)   # ablation bits / chunk log: development build
 prec = int(sys.argv[1])
 vals = [int(v) for v in sys.argv[2].split(",")]
 cfg = fd.MoeConfig(tokens_per_device=16384, embed_dim=2048, ffn_dim=2048, experts_total=128, devices=1, topk=2,

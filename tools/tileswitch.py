@@ -5,6 +5,7 @@ sys.path.insert(0, '.')
 import numpy as np
 import torch
 import paper_2506_04667_b200 as fd
+fd.select_library(fd._build.DEV_LIB)   # ablation bits / chunk log: development build
 prec = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 cfg = fd.MoeConfig(tokens_per_device=16384, embed_dim=2048, ffn_dim=2048, experts_total=128, devices=1, topk=2,
                    tile_rows=128, tile_cols=64, precision=prec)
