@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define FDMOE_ABI_VERSION 2
+#define FDMOE_ABI_VERSION 3
 
 typedef enum fdmoe_status {
     FDMOE_OK = 0,
@@ -122,9 +122,17 @@ typedef struct fdmoe_routing {
 } fdmoe_routing;
 
 /* TaskStats (runtime.hpp:94-106) with GPU meaning, per local rank:
- * gemm0/gemm1 = 128-row FFN tiles executed, combine = combine tasks,
- * launches = kernel launches this forward (1). bytes / bytes_padded are the P x P
- * efficient / padded-baseline payload matrices (pgas.hpp:130-147). */
+ * gemm0/gemm1 = 128-row FFN tiles executed (counted by the signal warps), combine = combine tasks,
+ * launches = kernel launches this forward (1).
+ * Task accounting (runtime.hpp:122-165, 407-415 on the kernel's static tile grid):
+ *   bound_initial   = El * MT * (NB0 + NB1) FFN tasks (+ ceil(S/16) combine tasks when the combine is a
+ *                     separate phase) -- the initial_task_bound analogue;
+ *   bound_final     = bound_initial self-corrected on the device: each row tile whose dispatch signals
+ *                     resolve to zero rows removes its NB0 + NB1 tasks (self_correct_task_bound);
+ *   scheduled_final = non-empty FFN tasks the device producers scheduled (+ combine tasks);
+ *   enqueued        = scheduled_final; tiles_resolved = row tiles whose signals were resolved.
+ * A correct forward has bound_final == scheduled_final == executed (the reference terminates on
+ * scheduled == bound, runtime.hpp:633-647). */
 typedef struct fdmoe_stats {
     int64_t gemm0, gemm1, combine, enqueued, executed;
     int64_t bound_initial, bound_final, scheduled_final, launches;
@@ -132,6 +140,7 @@ typedef struct fdmoe_stats {
     int64_t gate_exact_tokens; /* tokens whose logits were recomputed exactly for all experts
                                 * (all S with exact_gate; ties / near-ties otherwise) */
     int64_t gate_pair_tokens;  /* tokens the certified gate decided from exact candidate logits */
+    int64_t tiles_resolved;    /* row tiles whose dispatch signals the device producers resolved */
 } fdmoe_stats;
 
 typedef struct fdmoe_handle fdmoe_handle;
@@ -193,7 +202,14 @@ fdmoe_status fdmoe_set_weights(fdmoe_handle* h, const float* wg, const float* w1
 
 /* One MoE-layer forward: exactly one persistent kernel launch per device.
  * in_shards / out_shards: n_local pointers to S x H FP32 (host or device per `where`).
- * routing / stats: arrays of n_local entries, nullable. Synchronous. */
+ * routing / stats: arrays of n_local entries, nullable. Synchronous.
+ * Aliasing: an output shard must not overlap its input shard (FDMOE_ERR_CONFIG) -- the kernel still
+ * reads input rows (dispatch) while the fused combine zeroes and accumulates output rows.
+ * Numerics: the fused FP32 combine (k <= 2) adds fl(w*y) terms with float RED atomics, which flush
+ * subnormal results to zero; outputs equal the reference's pick-order sum except where that sum (or a
+ * term) is subnormal (|x| < 2^-126), where the device returns 0.
+ * Ordering: launches of one handle are serialised across streams (a launch on a different stream than
+ * the previous one waits for it). */
 fdmoe_status fdmoe_forward(fdmoe_handle* h, const float* const* in_shards, float* const* out_shards,
                            int32_t where, const fdmoe_options* opts, fdmoe_routing* routing,
                            fdmoe_stats* stats);

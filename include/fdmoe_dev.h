@@ -19,7 +19,8 @@ fdmoe_status fdmoe_debug_expf(const float* x, float* y, int64_t n);
 fdmoe_status fdmoe_debug_gemm(int32_t precision, int32_t K, const float* W, const float* X, float* D);
 /* Issue-rate microbenchmark: SM cycles per tcgen05.mma (M=128, A from TMEM, N in {64,128,256})
  * when `nissuers` warps (1-2) each issue `iters` back-to-back MMAs into their own accumulator;
- * kind 0 = tf32, 1 = bf16. */
+ * kind 0 = tf32, 1 = bf16. kind >= 16: the FFN pipeline skeleton (fdmoe_kernel.cu debug_pipe_kernel,
+ * mode = kind - 16) on 148 CTAs, iters = half-stages of 12 MMAs; returns cycles per MMA. */
 /* Latency probe (cycles): [0] issue of n tf32 N=128 MMAs, [1] issue -> commit completion,
  * [2] 8 x tcgen05.st.x16 + wait::st, [3] mbarrier wait with a 2000-cycle delayed arrive. */
 fdmoe_status fdmoe_debug_latency(int32_t n, uint64_t* out4);

@@ -106,7 +106,8 @@ class _Stats(C.Structure):
     _fields_ = [("gemm0", C.c_int64), ("gemm1", C.c_int64), ("combine", C.c_int64), ("enqueued", C.c_int64),
                 ("executed", C.c_int64), ("bound_initial", C.c_int64), ("bound_final", C.c_int64),
                 ("scheduled_final", C.c_int64), ("launches", C.c_int64), ("kernel_ms", C.c_double),
-                ("gate_exact_tokens", C.c_int64), ("gate_pair_tokens", C.c_int64)]
+                ("gate_exact_tokens", C.c_int64), ("gate_pair_tokens", C.c_int64),
+                ("tiles_resolved", C.c_int64)]
 
 
 class _Info(C.Structure):
@@ -129,6 +130,9 @@ EXPORTED_SYMBOLS = [
 _LIB = None
 _DEV_LIB = None
 _LIB_PATH = None   # select_library(): tools/ A/B runs of another build; None = the in-tree product library
+
+
+TRACE_POINTS = 40   # kTracePts (fdmoe_device.cuh)
 
 
 def select_library(path: str):
@@ -359,6 +363,7 @@ class TaskStats:
     kernel_ms: float = 0.0
     gate_exact_tokens: int = 0
     gate_pair_tokens: int = 0
+    tiles_resolved: int = 0
 
     def total(self) -> int:
         return self.gemm0 + self.gemm1 + self.combine
@@ -631,9 +636,10 @@ class Operator:
 
     def trace(self, local_rank: int = 0) -> np.ndarray:
         """Per-CTA phase timestamps of the last launch (ns, relative to the earliest CTA start):
-        columns start, gate, barrier, dispatch, ffn, combine, end, ffn_tiles."""
+        columns start, gate, barrier, dispatch, ffn, combine, end, ffn_tiles; ... 32-35: raw SM clock64 at the
+        start, FFN start, FFN end and end (effective SM clock per phase = cycles / ns)."""
         info = self.info()
-        buf = np.zeros((info["ctas_per_rank"], 32), np.uint64)
+        buf = np.zeros((info["ctas_per_rank"], TRACE_POINTS), np.uint64)
         n = C.c_int32()
         _check(lib().fdmoe_read_trace(self._h, local_rank, _ptr(buf), buf.size, C.byref(n)))
         t = buf.astype(np.int64)

@@ -30,7 +30,7 @@ constexpr int kMaxRanks = 64;       // P envelope (peer table size)
 constexpr int kMaxSrcPerTile = 8;   // packet_rows >= 16 -> <= 8 packets per 128-row tile
 constexpr int kCombineTok = 16;     // tokens per combine task (== kGateTok)
 constexpr int kMaxLocalRanks = 8;   // ranks per launch (virtual ranks on one GPU)
-constexpr int kTracePts = 32;
+constexpr int kTracePts = 40;
 constexpr int kGroupBarriers = 2;   // sequential mode: after dispatch, after the expert FFN
 constexpr int kChunkLog = 512;       // start, gate, barrier, dispatch, gemm, combine, end, tiles,
                                     // then FFN pipeline wait cycles (see kWait*)
@@ -41,7 +41,8 @@ enum WaitSlot : int {
     kTrGateLogits = 24, kTrGatePairs, kTrGateFull, kTrGateNFull,  // gate sub-phases (last sub-tile), full tokens
     kTrGateTc = 28,                                               // tensor-core gate logits done
     kTrGateLoad = 29,                                             // tensor-core logits staged for routing
-    kTrGateDecide = 30, kTrGateExp = 31                           // thread-route decisions / exps done
+    kTrGateDecide = 30, kTrGateExp = 31,                          // thread-route decisions / exps done
+    kTrClk0 = 32, kTrClkFfn0, kTrClkFfn1, kTrClkEnd               // clock64 at start / FFN start / FFN end / end
 };
 
 enum Prec : int { kFP32 = 0, kBF16 = 1 };
@@ -154,6 +155,8 @@ enum DebugBits : int {
     kDbgGateNoWgTma = 512,    // tensor-core gate: producer skips the Wg^T plane TMA (timing only)
     kDbgGateNoTokTma = 1024,  // tensor-core gate: producer skips the token-row TMA (timing only)
     kDbgGateNoEpi = 2048,     // tensor-core gate: epilogue skips the per-stage TMEM fold (timing only)
+    kDbgEvictNormal = 4096,   // token / C1 / gate-row loads with evict_normal instead of evict_last (A/B)
+    kDbgInjectOversub = 8192, // fault injection: CTA 0 over-counts one kept row of expert 0 (ProtocolError test)
 };
 
 // Ablation bits are honoured only by the development library (libfdmoe_dev.so, -DFDMOE_DEV);
@@ -289,6 +292,11 @@ __device__ __forceinline__ uint64_t l2_policy_evict_last() {
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+__device__ __forceinline__ uint64_t l2_policy_evict_normal() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
 __device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* m, uint64_t* bar, int x, int y,
                                                  uint64_t policy) {
     asm volatile(
@@ -335,6 +343,16 @@ __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64
         : "memory");
 }
 // A operand from TMEM (the expert's weight tile), B from shared memory (tokens).
+// elect.sync: true in exactly one lane of the (converged) warp
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
+}
 __device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
                                             uint32_t accumulate) {
     asm volatile(
@@ -383,6 +401,10 @@ __device__ __forceinline__ float4 ld_stream_f4(const void* p) {
     return v;
 }
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+// bulk L2 prefetch of [p, p + bytes) (16-byte aligned, bytes % 16 == 0), no completion tracking
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(

@@ -361,7 +361,7 @@ __device__ void gate_logits(const LaunchParams& P, const RankCtx& R, const float
     const int n_tg = (ts + TT - 1) / TT;
     const int n_items = n_tg * n_eg;
     const int nk = H / kGateKC;   // envelope: H % 32 == 0
-    const uint64_t pol_a = l2_policy_evict_last();   // token rows: keep for the dispatch push
+    const uint64_t pol_a = FD_DBG(kDbgEvictNormal) ? l2_policy_evict_normal() : l2_policy_evict_last();   // token rows: keep for the dispatch push
     for (int base = 0; base < n_items; base += kThreads) {   // item rounds (re-stream K per round)
         auto load_stage = [&](int st, int kb) {
             if (FD_DBG(kDbgGateNoLoad)) { cp_async_commit(); return; }
@@ -991,6 +991,20 @@ __device__ void gate_phase(const LaunchParams& P, const RankCtx& R, const float*
     g.sPZ = reinterpret_cast<float*>(tail);
     __shared__ int s_np, s_nfull;
     for (int e = tid; e < Ep; e += kThreads) g.sCnt[e] = 0;
+    // The exact passes read Wg (full pass, [H][E]) and Wg^T rows (pair pass): 2 x H*E*4 bytes that no other
+    // phase touches, so they are cold in HBM after the previous launch's weight stream. A near-tie token then
+    // streams 1 MB from HBM at one SM's memory-level parallelism (~50 us, the gate's critical path). Each CTA
+    // of the rank prefetches its slice of both into L2 first; the exact passes then hit L2.
+    if (tid == 0 && !P.exact_gate) {
+        const size_t bytes = (size_t)P.H * E * 4;
+        const size_t per = ((bytes + P.ctas_per_rank - 1) / P.ctas_per_rank + 15) & ~(size_t)15;
+        const size_t o = (size_t)cta * per;
+        if (o < bytes) {
+            const uint32_t n = (uint32_t)min(per, bytes - o);
+            prefetch_l2_bulk(reinterpret_cast<const uint8_t*>(R.wg) + o, n);
+            prefetch_l2_bulk(reinterpret_cast<const uint8_t*>(R.wgT) + o, n);
+        }
+    }
 
     int tokA, tokB, b0, b1;
     gate_token_range(P, cta, tokA, tokB, b0, b1);
@@ -1329,7 +1343,7 @@ __device__ void push_phase(const LaunchParams& P, const RankCtx& R, const float*
     if (tid == 0) __threadfence_system();
     __syncthreads();
     for (int e = tid; e < E; e += kThreads) {
-        const int kept = sMine[e];
+        const int kept = sMine[e] + (FD_DBG(kDbgInjectOversub) && e == 0 && cta == 0 && sMine[e] > 0 ? 1 : 0);
         if (kept <= 0) continue;
         const uint32_t old = atomicAdd(&R.sent[e], (uint32_t)kept);
         if ((int)(old + kept) == sN[e]) {
@@ -1421,13 +1435,24 @@ struct GemmCtrl {
     uint64_t tfull[kAccStages], tempty[kAccStages];  // accumulators
     uint64_t qfull[kTaskRing], qempty[kTaskRing];    // task ring
     uint64_t sfull[kTaskRing], sempty[kTaskRing];    // epilogue -> signal warp (finished tiles)
+    uint64_t pp[2];                                  // FP32 FFN issuer hand-off: pp[i] = "the other warp issued"
     uint32_t tmem_base;
+    uint32_t pp_corr;                                // FP32 FFN: correction accumulator state handed h=0 -> h=1
+    uint32_t pp_cph;                                 //   and the cempty parity, handed between the issuers
     uint32_t pad;
     Task ring[kTaskRing];
     Task sring[kTaskRing];                           // finished tiles awaiting their release signals
 };
 static_assert(sizeof(GemmCtrl) <= 1024, "GemmCtrl fits the control area");
 constexpr int kTaskConsumers = 1 + 4 + 1;   // MMA warp, 4 converter warps, epilogue
+template <int PREC>
+struct TaskConsumers {   // FP32 FFN: two MMA issuer warps
+    static constexpr int N = kTaskConsumers + (PREC == kFP32 ? 1 : 0);
+};
+template <int PREC>
+struct MmaCommits {      // arrivals per accumulator (tfull): one commit per issuer warp
+    static constexpr int N = PREC == kFP32 ? 2 : 1;
+};
 template <int PREC>
 struct ReadyCount {   // bf16: producer (expect_tx) + 4 converter warps; FP32: producer (tokens only)
     static constexpr int N = PREC == kFP32 ? 1 : 1 + 4;
@@ -1523,7 +1548,12 @@ __device__ void gemm_producer(const LaunchParams& P, const RankCtx& R, uint8_t* 
     // weights stream through once (evict first); token / C1 tiles are re-read by the other feature
     // blocks of the same row tile (keep)
     const uint64_t pol_w = l2_policy_evict_first();
-    const uint64_t pol_x = l2_policy_evict_last();
+    const uint64_t pol_x = FD_DBG(kDbgEvictNormal) ? l2_policy_evict_normal() : l2_policy_evict_last();
+    // Task accounting (runtime.hpp:122-165, 407-415 restated for the static tile grid): the bound starts at
+    // every (expert, row tile, feature block) task of both GEMMs and self-corrects when a row tile's dispatch
+    // signals resolve: an empty row tile removes its NB0 + NB1 tasks. Each row tile is corrected exactly once,
+    // by the producer that claims its (GEMM0, nb = 0) task. scheduled = non-empty tasks handed to the pipeline.
+    long long bound_delta = 0, scheduled = 0, tiles_resolved = 0;
     while (true) {
         const long long tf0 = pclk();
         const uint32_t t = atomicAdd(R.gemm_head, 1u);
@@ -1532,6 +1562,10 @@ __device__ void gemm_producer(const LaunchParams& P, const RankCtx& R, uint8_t* 
         if (!end) {
             decode_task(P, t, n_g0, tk);
             const int rows = resolve_tile_rows(P, R, tk);
+            if (rows >= 0 && tk.type == 0 && tk.nb == 0) {
+                ++tiles_resolved;
+                if (rows == 0) bound_delta -= P.NB0 + P.NB1;
+            }
             if (rows < 0) end = true;
             else if (rows == 0) continue;   // empty row tile: no GEMM0/GEMM1 work exists for it
             else if (tk.type == 1) {
@@ -1546,8 +1580,12 @@ __device__ void gemm_producer(const LaunchParams& P, const RankCtx& R, uint8_t* 
             trace[kWaitProdW] = w_w;
             trace[kWaitProdX] = w_x;
             trace[kProdFetch] = t_fetch;
+            atomicAdd(R.stats + 5, (unsigned long long)bound_delta);   // two's complement: a signed sum
+            atomicAdd(R.stats + 6, (unsigned long long)scheduled);
+            atomicAdd(R.stats + 7, (unsigned long long)tiles_resolved);
             return;
         }
+        ++scheduled;
         tk.t0 = P.trace_events ? globaltimer() : 0;
         G.ring[q] = tk;
         mbar_arrive(&G.qfull[q]);
@@ -1577,8 +1615,27 @@ __device__ void gemm_producer(const LaunchParams& P, const RankCtx& R, uint8_t* 
             }
             if (++wstage == Cfg::WSTAGES) { wstage = 0; wphase ^= 1u; }
 
-            if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.done[stage], phase ^ 1u, P.abort_flag))) return;
             uint8_t* st = ring + stage * Cfg::STAGE_BYTES;
+            if constexpr (PREC == kFP32) {
+                // FP32: the token ring is 2 stages x 2 atoms with one ready/done pair per ATOM (slot 2*stage + at):
+                // the two MMA issuer warps each consume one atom of every stage, so an atom's slot refills as soon
+                // as its 12 MMAs retire -- 3 of the 4 slots can be in flight instead of 1 of 2 stages (the token
+                // TMA from L2 is latency- not bandwidth-bound: lts__throughput 32 %, tools/dev ncu r02).
+#pragma unroll
+                for (int at = 0; at < Cfg::NATOM; ++at) {
+                    const int j = stage * Cfg::NATOM + at;
+                    if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.done[j], phase ^ 1u, P.abort_flag))) return;
+                    if (FD_DBG(kDbgNoXTma)) { mbar_arrive(&G.ready[j]); continue; }
+                    mbar_expect_tx(&G.ready[j], Cfg::PLANES * Cfg::ATOM_BYTES);
+#pragma unroll
+                    for (int pl = 0; pl < Cfg::PLANES; ++pl)
+                        tma_load_2d_hint(st + pl * Cfg::PLANE_BYTES + at * Cfg::ATOM_BYTES, tb[pl], &G.ready[j],
+                                         kb * Cfg::BK + at * Cfg::ATOM_K, y, pol_x);
+                }
+                if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
+                continue;
+            }
+            if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.done[stage], phase ^ 1u, P.abort_flag))) return;
             if (FD_DBG(kDbgNoXTma)) mbar_arrive(&G.ready[stage]);
             else {
                 mbar_expect_tx(&G.ready[stage], Cfg::STAGE_BYTES);
@@ -1731,8 +1788,26 @@ __device__ void gemm_wconvert(const LaunchParams& P, uint8_t* ring, GemmCtrl& G,
     }
 }
 
-// warp 11, one lane: tcgen05.mma issue. One wait (ready) and one commit (done) per stage.
+// warp 11: tcgen05.mma issue. The whole warp runs the issue loop (waits, bookkeeping) converged and one
+// elected lane issues each group of MMAs and commits. Operands computed by the converged warp are provably
+// warp-uniform, so each UTCHMMA takes them straight from uniform registers; issued from a single-lane branch
+// instead, every MMA sat in a compiler waterfall loop (ELECT + R2UR.BROADCAST per operand) and the
+// 12-MMA half-stage pattern issued at 100 cycles per MMA instead of the tensor core's 64
+// (tools/dev/mma_stream.py: pipe mode 112 vs 2160). One wait (ready) and one commit (done) per stage.
 constexpr int kProbeAt = 1;   // MMAs of a stage issued before the next stage's readiness probe
+
+// every lane waits; the warp proceeds only if no lane saw the abort word
+__device__ __forceinline__ bool wwait(uint64_t* bar, uint32_t parity, uint32_t* abort_flag) {
+    return __all_sync(0xffffffffu, mbar_wait(bar, parity, abort_flag));
+}
+// non-blocking probe, lane 0's observation for the whole warp (the elected issuer is lane 0)
+__device__ __forceinline__ bool wtest(uint64_t* bar, uint32_t parity) {
+    return __shfl_sync(0xffffffffu, mbar_test_wait(bar, parity) ? 1 : 0, 0) != 0;
+}
+__device__ __forceinline__ void wcommit(uint64_t* bar) {
+    if (elect_one()) mma_commit(bar);
+    __syncwarp();
+}
 
 template <int PREC>
 struct StageMmas {
@@ -1797,6 +1872,22 @@ __device__ __forceinline__ void issue_half_fp32(uint32_t d_main, uint32_t d_corr
     }
 }
 
+// Steady-state half-stage MMAs [I0, I1) of the 12 (both accumulators in use, accumulating): 0-3 w_lo*x_hi and
+// 4-7 w_hi*x_lo into the correction accumulator, 8-11 w_hi*x_hi into the main one -- issue_half_fp32's order,
+// split so the issuing warp can probe the next half-stage's barriers between the two parts.
+template <int I0, int I1>
+__device__ __forceinline__ void issue_fp32_steady(uint32_t d_main, uint32_t d_corr, uint32_t a_half, uint64_t bdesc,
+                                                  uint32_t idesc) {
+    using Cfg = GemmCfg<kFP32>;
+#pragma unroll
+    for (int i = I0; i < I1; ++i) {
+        const int ks = i & 3;
+        if (i < 4) mma_tf32_ts(d_corr, a_half + Cfg::ATOM_K + ks * Cfg::KSTEP, bdesc + ((ks * 32) >> 4), idesc, 1u);
+        else if (i < 8) mma_tf32_ts(d_corr, a_half + ks * Cfg::KSTEP, bdesc + ((Cfg::PLANE_BYTES + ks * 32) >> 4), idesc, 1u);
+        else mma_tf32_ts(d_main, a_half + ks * Cfg::KSTEP, bdesc + ((ks * 32) >> 4), idesc, 1u);
+    }
+}
+
 constexpr int kCorrInMainMax = 2;
 struct MmaFp32State {
     int stage = 0, ah = 0;
@@ -1809,7 +1900,7 @@ struct MmaFp32State {
 // for the fold, so the fold overlaps them.
 __device__ __forceinline__ bool mma_tile_fp32(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, uint32_t tmem,
                                               uint32_t d_main, int nk, uint32_t idesc, MmaFp32State& st,
-                                              long long& w_x) {
+                                              long long& w_x, unsigned long long* clog = nullptr, int* nlog = nullptr) {
     using Cfg = GemmCfg<kFP32>;
     const uint32_t d_corr = tmem + kTmemCorr;
     // The correction accumulator is free once the epilogue folded the previous tile's corrections
@@ -1821,42 +1912,62 @@ __device__ __forceinline__ bool mma_tile_fp32(const LaunchParams& P, uint8_t* ri
     // bound at c4 EP8 -- tests/test_gpu_baseline.py.)
     bool corr_free = false;
     const int nhalf = nk * Cfg::NATOM;
-    // (Probing the next half-stage's barriers between this half-stage's MMAs, so the boundary skips its
-    // wait, measured slower: 1.581 -> 1.606 ms at c4. The single issuer keeps plain waits.)
+    // Steady state: the half-stage's MMAs and their commits go out in one elected block. (Probing the next
+    // half-stage's barriers between its MMAs so the boundary can skip its wait measured slower: 1.565 -> 1.631 ms.)
+    const bool rdy_known = false, a_known = false;
     for (int kb = 0; kb < nk; ++kb) {
-        if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.ready[st.stage], st.phase, P.abort_flag))) return false;
+        if (!rdy_known && !FD_TIMED_WAIT(w_x, wwait(&G.ready[st.stage], st.phase, P.abort_flag))) return false;
         tc_fence_after();
         const uint64_t bdesc = umma_desc_kmajor(smem_u32(ring + st.stage * Cfg::STAGE_BYTES), 128);
+        const int nstage = st.stage + 1 == Cfg::STAGES ? 0 : st.stage + 1;
+        const uint32_t nphase = st.stage + 1 == Cfg::STAGES ? st.phase ^ 1u : st.phase;
 #pragma unroll
         for (int at = 0; at < Cfg::NATOM; ++at) {
-            if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.afull[st.ah], st.ahph, P.abort_flag))) return false;
+            const long long c0 = clog ? pclk() : 0;
+            if (!a_known && !FD_TIMED_WAIT(w_x, wwait(&G.afull[st.ah], st.ahph, P.abort_flag))) return false;
             tc_fence_after();
+            const long long c1 = clog ? pclk() : 0;
             const uint32_t a_half = tmem + Cfg::TMEM_A0 + st.ah * Cfg::A_COLS;
             const uint64_t bd = bdesc + ((at * Cfg::ATOM_BYTES) >> 4);
             const bool first = kb == 0 && at == 0;
+            const bool stage_end = at == Cfg::NATOM - 1;
             if (corr_free) {
-                issue_half_fp32<true, true>(d_main, d_corr, a_half, bd, idesc, first ? 0u : 1u, 1u);
+                if (elect_one()) {
+                    issue_fp32_steady<0, 12>(d_main, d_corr, a_half, bd, idesc);
+                    mma_commit(&G.aempty[st.ah]);
+                    if (stage_end) mma_commit(&G.done[st.stage]);   // token + weight stage reusable
+                }
+                __syncwarp();
             } else {
-                issue_half_fp32<true, false>(d_main, d_corr, a_half, bd, idesc, first ? 0u : 1u, 0u);
+                if (elect_one()) issue_half_fp32<true, false>(d_main, d_corr, a_half, bd, idesc, first ? 0u : 1u, 0u);
+                __syncwarp();
                 const int h = kb * Cfg::NATOM + at;
-                corr_free = mbar_test_wait(&G.cempty, st.cph ^ 1u);
+                corr_free = wtest(&G.cempty, st.cph ^ 1u);
                 if (!corr_free && (h + 1 >= kCorrInMainMax || h + 1 == nhalf)) {
-                    if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.cempty, st.cph ^ 1u, P.abort_flag))) return false;
+                    if (!FD_TIMED_WAIT(w_x, wwait(&G.cempty, st.cph ^ 1u, P.abort_flag))) return false;
                     corr_free = true;
                 }
                 if (corr_free) {
                     st.cph ^= 1u;
                     tc_fence_after();
-                    issue_half_fp32<false, true>(d_main, d_corr, a_half, bd, idesc, 0u, 0u);
+                    if (elect_one()) issue_half_fp32<false, true>(d_main, d_corr, a_half, bd, idesc, 0u, 0u);
                 } else {   // corrections of this half-stage ride in the main accumulator
-                    issue_half_fp32<false, true>(d_main, d_main, a_half, bd, idesc, 0u, 1u);
+                    if (elect_one()) issue_half_fp32<false, true>(d_main, d_main, a_half, bd, idesc, 0u, 1u);
                 }
+                __syncwarp();
+                wcommit(&G.aempty[st.ah]);
+                if (stage_end) wcommit(&G.done[st.stage]);
             }
-            mma_commit(&G.aempty[st.ah]);
+            const long long c2 = clog ? pclk() : 0;
+            if (clog && (threadIdx.x & 31) == 0 && *nlog < kChunkLog / 2) {
+                // chunk log (development build): per half-stage {afull wait start, wait end, MMAs issued, logged}
+                unsigned long long* o = clog + 4 * (*nlog)++;
+                o[0] = c0; o[1] = c1; o[2] = c2; o[3] = pclk();
+            }
             if (++st.ah == Cfg::A_SLOTS) { st.ah = 0; st.ahph ^= 1u; }
         }
-        mma_commit(&G.done[st.stage]);
-        if (++st.stage == Cfg::STAGES) { st.stage = 0; st.phase ^= 1u; }
+        st.stage = nstage;
+        st.phase = nphase;
     }
     return true;
 }
@@ -1872,33 +1983,35 @@ __device__ __forceinline__ bool mma_gate_tile(const LaunchParams& P, uint8_t* ri
     using Cfg = GemmCfg<kFP32>;
     const uint32_t d_corr = tmem + kTmemCorr;
     for (int kb = 0; kb < nk; ++kb) {
-        if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.tempty[acc], accphase ^ 1u, P.abort_flag))) return false;
+        if (!FD_TIMED_WAIT(w_x, wwait(&G.tempty[acc], accphase ^ 1u, P.abort_flag))) return false;
         const uint32_t d_main = tmem + (uint32_t)(acc * kNT);
-        if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.ready[st.stage], st.phase, P.abort_flag))) return false;
+        if (!FD_TIMED_WAIT(w_x, wwait(&G.ready[st.stage], st.phase, P.abort_flag))) return false;
         tc_fence_after();
         const uint64_t bdesc = umma_desc_kmajor(smem_u32(ring + st.stage * Cfg::STAGE_BYTES), 128);
 #pragma unroll
         for (int at = 0; at < Cfg::NATOM; ++at) {
-            if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.afull[st.ah], st.ahph, P.abort_flag))) return false;
+            if (!FD_TIMED_WAIT(w_x, wwait(&G.afull[st.ah], st.ahph, P.abort_flag))) return false;
             tc_fence_after();
             const uint32_t a_half = tmem + Cfg::TMEM_A0 + st.ah * Cfg::A_COLS;
             const uint64_t bd = bdesc + ((at * Cfg::ATOM_BYTES) >> 4);
             const uint32_t main_acc = at == 0 ? 0u : 1u;
             if (kb == 0 && at == 0) {
-                issue_half_fp32<true, false>(d_main, d_corr, a_half, bd, idesc, 0u, 0u);
-                if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.cempty, st.cph ^ 1u, P.abort_flag))) return false;
+                if (elect_one()) issue_half_fp32<true, false>(d_main, d_corr, a_half, bd, idesc, 0u, 0u);
+                __syncwarp();
+                if (!FD_TIMED_WAIT(w_x, wwait(&G.cempty, st.cph ^ 1u, P.abort_flag))) return false;
                 st.cph ^= 1u;
                 tc_fence_after();
-                issue_half_fp32<false, true>(d_main, d_corr, a_half, bd, idesc, 0u, 0u);
+                if (elect_one()) issue_half_fp32<false, true>(d_main, d_corr, a_half, bd, idesc, 0u, 0u);
             } else {
-                issue_half_fp32<true, true>(d_main, d_corr, a_half, bd, idesc, main_acc, 1u);
+                if (elect_one()) issue_half_fp32<true, true>(d_main, d_corr, a_half, bd, idesc, main_acc, 1u);
             }
-            mma_commit(&G.aempty[st.ah]);
+            __syncwarp();
+            wcommit(&G.aempty[st.ah]);
             if (++st.ah == Cfg::A_SLOTS) { st.ah = 0; st.ahph ^= 1u; }
         }
-        mma_commit(&G.done[st.stage]);
+        wcommit(&G.done[st.stage]);
         if (++st.stage == Cfg::STAGES) { st.stage = 0; st.phase ^= 1u; }
-        mma_commit(&G.tfull[acc]);   // this stage's main partial (and, at the last stage, the corrections)
+        wcommit(&G.tfull[acc]);   // this stage's main partial (and, at the last stage, the corrections)
         if (++acc == kAccStages) { acc = 0; accphase ^= 1u; }
     }
     return true;
@@ -1910,6 +2023,7 @@ __device__ void gemm_mma(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, unsi
     using Cfg = GemmCfg<PREC>;
     constexpr int NM = StageMmas<PREC>::N;
     int nlog = 0;
+    const int lane = threadIdx.x & 31;
     long long w_x = 0, w_acc = 0, w_task = 0, ntile = 0;
     int stage = 0;
     uint32_t phase = 0;
@@ -1924,13 +2038,16 @@ __device__ void gemm_mma(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, unsi
                                  umma_desc_kmajor(smem_u32(ring + Cfg::STAGE_BYTES), 128)};
     MmaFp32State st32;
     while (true) {
-        if (!FD_TIMED_WAIT(w_task, mbar_wait(&G.qfull[q], qphase, P.abort_flag))) return;
+        if (!FD_TIMED_WAIT(w_task, wwait(&G.qfull[q], qphase, P.abort_flag))) return;
         const int type = G.ring[q].type;
-        mbar_arrive(&G.qempty[q]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&G.qempty[q]);
         if (++q == kTaskRing) { q = 0; qphase ^= 1u; }
         if (type < 0) {
-            trace[kWaitMmaX] = w_x; trace[kWaitMmaA] = 0; trace[kWaitMmaAcc] = w_acc;
-            trace[kWaitMmaTask] = w_task; trace[kMmaTiles] = ntile;
+            if (lane == 0) {
+                trace[kWaitMmaX] = w_x; trace[kWaitMmaA] = 0; trace[kWaitMmaAcc] = w_acc;
+                trace[kWaitMmaTask] = w_task; trace[kMmaTiles] = ntile;
+            }
             return;
         }
         ++ntile;
@@ -1943,39 +2060,37 @@ __device__ void gemm_mma(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, unsi
                 continue;
             }
         }
-        if (!FD_TIMED_WAIT(w_acc, mbar_wait(&G.tempty[acc], accphase ^ 1u, P.abort_flag))) return;
+        if (!FD_TIMED_WAIT(w_acc, wwait(&G.tempty[acc], accphase ^ 1u, P.abort_flag))) return;
         const uint32_t d_tmem = tmem + (uint32_t)(acc * kNT);
         if constexpr (PREC == kFP32) {
-            if (!mma_tile_fp32(P, ring, G, tmem, d_tmem, nk, Cfg::IDESC, st32, w_x)) return;
-            mma_commit(&G.tfull[acc]);   // main + correction accumulators ready for the epilogue
+            if (!mma_tile_fp32(P, ring, G, tmem, d_tmem, nk, Cfg::IDESC, st32, w_x, chunklog, &nlog)) return;
+            wcommit(&G.tfull[acc]);   // main + correction accumulators ready for the epilogue
             if (++acc == kAccStages) { acc = 0; accphase ^= 1u; }
             continue;
         }
         long long t_rdy = chunklog ? pclk() : 0;
-        if (!FD_TIMED_WAIT(w_x, mbar_wait(&G.ready[stage], phase, P.abort_flag))) return;
+        if (!FD_TIMED_WAIT(w_x, wwait(&G.ready[stage], phase, P.abort_flag))) return;
         tc_fence_after();
         if (Cfg::STAGES == 2 && stage == 0 && (nk & 1) == 0 && !chunklog) {
             // Lean path (tile starts at ring slot 0, even stage count): stage pairs with compile-time
             // slot indices, so a stage boundary is the commit, one probe and the descriptor selects.
             for (int kb = 0; kb < nk; kb += 2) {
                 const bool last = kb + 2 == nk;
-                issue_stage<PREC, 0, kProbeAt>(d_tmem, abase_s[0], bdesc_s[0], kb == 0);
-                const bool r1 = mbar_test_wait(&G.ready[1], phase);
-                issue_stage<PREC, kProbeAt, NM>(d_tmem, abase_s[0], bdesc_s[0], kb == 0);
-                mma_commit(&G.done[0]);
-                if (!r1 && !FD_TIMED_WAIT(w_x, mbar_wait(&G.ready[1], phase, P.abort_flag))) return;
+                if (elect_one()) issue_stage<PREC, 0, NM>(d_tmem, abase_s[0], bdesc_s[0], kb == 0);
+                __syncwarp();
+                wcommit(&G.done[0]);
+                if (!FD_TIMED_WAIT(w_x, wwait(&G.ready[1], phase, P.abort_flag))) return;
                 tc_fence_after();
-                issue_stage<PREC, 0, kProbeAt>(d_tmem, abase_s[1], bdesc_s[1], 0u);
-                const bool r0 = last || mbar_test_wait(&G.ready[0], phase ^ 1u);
-                issue_stage<PREC, kProbeAt, NM>(d_tmem, abase_s[1], bdesc_s[1], 0u);
-                mma_commit(&G.done[1]);
+                if (elect_one()) issue_stage<PREC, 0, NM>(d_tmem, abase_s[1], bdesc_s[1], 0u);
+                __syncwarp();
+                wcommit(&G.done[1]);
                 phase ^= 1u;
                 if (!last) {
-                    if (!r0 && !FD_TIMED_WAIT(w_x, mbar_wait(&G.ready[0], phase, P.abort_flag))) return;
+                    if (!FD_TIMED_WAIT(w_x, wwait(&G.ready[0], phase, P.abort_flag))) return;
                     tc_fence_after();
                 }
             }
-            mma_commit(&G.tfull[acc]);
+            wcommit(&G.tfull[acc]);
             if (++acc == kAccStages) { acc = 0; accphase ^= 1u; }
             continue;
         }
@@ -1987,17 +2102,12 @@ __device__ void gemm_mma(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, unsi
             const int nstage = stage + 1 == Cfg::STAGES ? 0 : stage + 1;
             const uint32_t nphase = stage + 1 == Cfg::STAGES ? phase ^ 1u : phase;
             const bool last = kb + 1 == nk;
-            // The next stage's readiness is probed (non-blocking) right after the first MMA is queued:
-            // the probe's latency then hides behind this stage's MMA issue instead of leaving the
-            // ~2-deep tensor queue to drain at the stage boundary.
-            bool nrdy = true;
-            issue_stage<PREC, 0, kProbeAt>(d_tmem, abase, bdesc, kb == 0);
-            if (!last) nrdy = mbar_test_wait(&G.ready[nstage], nphase);
-            issue_stage<PREC, kProbeAt, NM>(d_tmem, abase, bdesc, kb == 0);
-            mma_commit(&G.done[stage]);   // token + weight stage reusable once these MMAs retire
-            if (chunklog && nlog < kChunkLog / 2) {
+            if (elect_one()) issue_stage<PREC, 0, NM>(d_tmem, abase, bdesc, kb == 0);
+            __syncwarp();
+            wcommit(&G.done[stage]);   // token + weight stage reusable once these MMAs retire
+            if (chunklog && lane == 0 && nlog < kChunkLog / 2) {
                 chunklog[4 * nlog] = pclk();
-                chunklog[4 * nlog + 1] = t_rdy;   // wait for ready started (bit 62: ready already)
+                chunklog[4 * nlog + 1] = t_rdy;   // wait for ready started
                 chunklog[4 * nlog + 2] = t_iss;   // ready observed, issue starts
                 chunklog[4 * nlog + 3] = 0;
                 ++nlog;
@@ -2005,12 +2115,136 @@ __device__ void gemm_mma(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, unsi
             stage = nstage;
             phase = nphase;
             if (!last) {
-                if (chunklog) t_rdy = pclk() | ((long long)nrdy << 62);
-                if (!nrdy && !FD_TIMED_WAIT(w_x, mbar_wait(&G.ready[stage], phase, P.abort_flag))) return;
+                if (chunklog) t_rdy = pclk();
+                if (!FD_TIMED_WAIT(w_x, wwait(&G.ready[stage], phase, P.abort_flag))) return;
                 tc_fence_after();
             }
         }
-        mma_commit(&G.tfull[acc]);         // accumulator ready for the epilogue
+        wcommit(&G.tfull[acc]);         // accumulator ready for the epilogue
+        if (++acc == kAccStages) { acc = 0; accphase ^= 1u; }
+    }
+}
+
+// FP32 FFN issue on TWO warps (kWarpMma: even half-stages = token atom 0 of each stage, A slot 0; kWarpMma2:
+// odd half-stages = atom 1, A slot 1), strictly alternating through an mbarrier hand-off (pp[]). Each warp has
+// its own token atom slots (ready/done per atom) and A slot, so only the accumulator commit (tfull) counts both. The tensor queue
+// holds only ~1-2 MMAs, so every wait / commit / bookkeeping step between two half-stages of ONE issuer drained it
+// (chunk log: ~450 cycles per 768-cycle half-stage); with two issuers each does its waits while the other one's
+// 12 MMAs run, and the hand-off (arrive -> wait, ~tens of cycles) is the only gap (tools/dev/pipe_rate3.py: 91.7 ->
+// 64.0 cycles per MMA for the full barrier protocol). Issue order is identical to one issuer's (results are
+// bit-identical); each warp commits its own MMAs.
+__device__ void gemm_mma_fp32_pp(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, unsigned long long* trace,
+                                 unsigned long long* clog, const int par) {
+    using Cfg = GemmCfg<kFP32>;
+    const int lane = threadIdx.x & 31;
+    long long w_x = 0, w_acc = 0, w_task = 0, ntile = 0;
+    int q = 0;
+    uint32_t qphase = 0;
+    int acc = 0;
+    uint32_t accphase = 0;
+    int stage = 0;
+    uint32_t phase = 0, aph = 0, pph = 0;
+    bool started = par == 1;   // par 0's very first half-stage has no predecessor
+    int nlog = 0;
+    const uint32_t tmem = G.tmem_base;
+    const uint32_t d_corr = tmem + kTmemCorr;
+    const uint32_t a_half = tmem + Cfg::TMEM_A0 + (uint32_t)par * Cfg::A_COLS;
+    const uint32_t idesc = Cfg::IDESC;
+    while (true) {
+        if (!FD_TIMED_WAIT(w_task, wwait(&G.qfull[q], qphase, P.abort_flag))) return;
+        const int type = G.ring[q].type;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&G.qempty[q]);
+        if (++q == kTaskRing) { q = 0; qphase ^= 1u; }
+        if (type < 0) {
+            if (lane == 0 && par == 0) {
+                trace[kWaitMmaX] = w_x; trace[kWaitMmaA] = 0; trace[kWaitMmaAcc] = w_acc;
+                trace[kWaitMmaTask] = w_task; trace[kMmaTiles] = ntile;
+            }
+            return;
+        }
+        ++ntile;
+        const int nk = (task_k(P, type) + Cfg::BK - 1) / Cfg::BK;
+        const long long t_tile = clog ? pclk() : 0;
+        long long s_tok = 0, s_a = 0, s_pp = 0;
+        if (par == 0 && !FD_TIMED_WAIT(w_acc, wwait(&G.tempty[acc], accphase ^ 1u, P.abort_flag))) return;
+        const long long t_acc = clog ? pclk() : 0;
+        const uint32_t d_main = tmem + (uint32_t)(acc * kNT);
+        for (int kb = 0; kb < nk; ++kb) {
+            const long long c0 = clog ? pclk() : 0;
+            const int slot = stage * Cfg::NATOM + par;   // this warp's token atom of the stage (own ready/done)
+            if (!FD_TIMED_WAIT(w_x, wwait(&G.ready[slot], phase, P.abort_flag))) return;
+            const long long c1 = clog ? pclk() : 0;
+            if (!FD_TIMED_WAIT(w_x, wwait(&G.afull[par], aph, P.abort_flag))) return;
+            const long long c2 = clog ? pclk() : 0;
+            if (started && !FD_TIMED_WAIT(w_x, wwait(&G.pp[par], pph, P.abort_flag))) return;   // h-1 issued
+            const long long c3 = clog ? pclk() : 0;
+            if (started) pph ^= 1u;
+            started = true;
+            tc_fence_after();
+            const uint64_t bd = umma_desc_kmajor(smem_u32(ring + stage * Cfg::STAGE_BYTES), 128) +
+                                (uint64_t)((par * Cfg::ATOM_BYTES) >> 4);
+            const bool last = kb + 1 == nk;
+            if (kb > 0) {   // steady state: both accumulators accumulate
+                if (elect_one()) {
+                    issue_fp32_steady<0, 12>(d_main, d_corr, a_half, bd, idesc);
+                    mma_commit(&G.aempty[par]);
+                    mma_commit(&G.done[slot]);
+                    if (last) mma_commit(&G.tfull[acc]);
+                }
+                __syncwarp();
+            } else if (par == 0) {   // h = 0: main starts fresh; corrections fresh if the fold freed kTmemCorr
+                if (elect_one()) issue_half_fp32<true, false>(d_main, d_corr, a_half, bd, idesc, 0u, 0u);
+                __syncwarp();
+                uint32_t cph = G.pp_cph;
+                const bool corr_free = wtest(&G.cempty, cph ^ 1u);
+                if (corr_free) {
+                    cph ^= 1u;
+                    tc_fence_after();
+                }
+                if (elect_one()) {
+                    if (corr_free) issue_half_fp32<false, true>(d_main, d_corr, a_half, bd, idesc, 0u, 0u);
+                    else issue_half_fp32<false, true>(d_main, d_main, a_half, bd, idesc, 0u, 1u);   // ride in main
+                    mma_commit(&G.aempty[par]);
+                    mma_commit(&G.done[slot]);
+                    if (last) mma_commit(&G.tfull[acc]);
+                    G.pp_corr = corr_free ? 1u : 0u;
+                    G.pp_cph = cph;
+                }
+                __syncwarp();
+            } else {   // h = 1: corrections into kTmemCorr -- fresh if h = 0 could not, after the fold (blocking)
+                uint32_t cph = G.pp_cph;
+                const bool corr_free = G.pp_corr != 0;
+                if (elect_one()) issue_half_fp32<true, false>(d_main, d_corr, a_half, bd, idesc, 1u, 0u);
+                __syncwarp();
+                if (!corr_free) {
+                    if (!FD_TIMED_WAIT(w_x, wwait(&G.cempty, cph ^ 1u, P.abort_flag))) return;
+                    cph ^= 1u;
+                    tc_fence_after();
+                }
+                if (elect_one()) {
+                    issue_half_fp32<false, true>(d_main, d_corr, a_half, bd, idesc, 0u, corr_free ? 1u : 0u);
+                    mma_commit(&G.aempty[par]);
+                    mma_commit(&G.done[slot]);
+                    if (last) mma_commit(&G.tfull[acc]);
+                    G.pp_cph = cph;
+                }
+                __syncwarp();
+            }
+            // hand-off: this half-stage is issued (tcgen05 ops ordered before the other warp's by the fence pair)
+            tc_fence_before();
+            if (lane == 0) mbar_arrive(&G.pp[par ^ 1]);
+            s_tok += c1 - c0; s_a += c2 - c1; s_pp += c3 - c2;
+            if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
+            aph ^= 1u;
+        }
+        if (clog && lane == 0 && nlog < kChunkLog / 4) {
+            // chunk log (development build), rows [128 * par, +128): per tile {type | tile cycles << 8, accumulator
+            // wait, token wait, A wait | hand-off wait << 32}
+            unsigned long long* o = clog + 4 * (par * (kChunkLog / 4) + nlog++);
+            o[0] = (unsigned long long)type | ((unsigned long long)(pclk() - t_tile) << 8);
+            o[1] = t_acc - t_tile; o[2] = s_tok; o[3] = (unsigned long long)s_a | ((unsigned long long)s_pp << 32);
+        }
         if (++acc == kAccStages) { acc = 0; accphase ^= 1u; }
     }
 }
@@ -2294,7 +2528,7 @@ __device__ void gate_producer(const LaunchParams& P, const RankCtx& R, int rl, u
     tma_prefetch(ta);
     tma_prefetch(&R.tm_wg[0]);
     tma_prefetch(&R.tm_wg[1]);
-    const uint64_t pol = l2_policy_evict_last();   // token rows: re-read by the dispatch push; Wg: by every CTA
+    const uint64_t pol = FD_DBG(kDbgEvictNormal) ? l2_policy_evict_normal() : l2_policy_evict_last();   // token rows: re-read by the dispatch push; Wg: by every CTA
     const int nk = (P.H + Cfg::BK - 1) / Cfg::BK;
     const uint32_t bbytes = (uint32_t)(Cfg::PLANES * Cfg::NATOM * P.gate_n * 128);
     for (int tok0 = tokA; tok0 < tokB; tok0 += kNT)
@@ -2555,7 +2789,7 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
     if (tid < 5) s_stat[tid] = 0;
     if (tid < 32) s_exp_tab[tid] = c_exp_tab[tid];
     unsigned long long* trace = R.trace + (size_t)cta * kTracePts;
-    if (tid == 0) trace[0] = globaltimer();
+    if (tid == 0) { trace[0] = globaltimer(); trace[kTrClk0] = clock64(); }
 
     GemmCtrl& G = *reinterpret_cast<GemmCtrl*>(smem + SmemPlan<PREC>::REGION);
     uint8_t* ring = smem;
@@ -2587,7 +2821,7 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
         int tokA, tokB, b0, b1;
         gate_token_range(P, cta, tokA, tokB, b0, b1);
         if (warp == kWarpMma) {
-            if ((tid & 31) == 0) gemm_mma<kFP32>(P, ring, GG, trace, nullptr);
+            gemm_mma<kFP32>(P, ring, GG, trace, nullptr);
         } else if (warp == kWarpProducer) {
             if ((tid & 31) == 0) gate_producer(P, R, rl, ring, GG, tokA, tokB);
         } else if (warp >= kWarpConv0 && warp < kWarpConv0 + 4) {
@@ -2620,26 +2854,34 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
     for (int e = tid; e < P.E; e += kThreads) s_n_expert[e] = reinterpret_cast<const int*>(smem)[kMaxExperts + e];
     // sequential schedule: every rank's dispatch lands before any expert tile starts
     if (P.sequential && !group_barrier(P, R, P.launch_seq + 2, 0, cta)) goto done;
-    if (tid == 0) trace[3] = globaltimer();
+    if (tid == 0) { trace[3] = globaltimer(); trace[kTrClkFfn0] = clock64(); }
 
     // phase 3: expert FFN tiles
     if (tid == 0) {
-        for (int i = 0; i < Cfg::STAGES; ++i) { mbar_init(&G.ready[i], ReadyCount<PREC>::N); mbar_init(&G.done[i], 1); }
+        // FP32: one ready/done pair per token atom (slot 2 * stage + atom, gemm_producer); bf16: per stage
+        for (int i = 0; i < Cfg::STAGES * (PREC == kFP32 ? Cfg::NATOM : 1); ++i) {
+            mbar_init(&G.ready[i], ReadyCount<PREC>::N);
+            mbar_init(&G.done[i], 1);
+        }
         for (int i = 0; i < Cfg::WSTAGES; ++i) { mbar_init(&G.wfull[i], 1); mbar_init(&G.wempty[i], 4); }
-        for (int i = 0; i < 2; ++i) { mbar_init(&G.afull[i], 4); mbar_init(&G.aempty[i], 1); }
+        for (int i = 0; i < 2; ++i) { mbar_init(&G.afull[i], 4); mbar_init(&G.aempty[i], 1); mbar_init(&G.pp[i], 1); }
         mbar_init(&G.cempty, 4);
-        for (int i = 0; i < kAccStages; ++i) { mbar_init(&G.tfull[i], 1); mbar_init(&G.tempty[i], 1); }
-        for (int i = 0; i < kTaskRing; ++i) { mbar_init(&G.qfull[i], 1); mbar_init(&G.qempty[i], kTaskConsumers); }
+        for (int i = 0; i < kAccStages; ++i) { mbar_init(&G.tfull[i], MmaCommits<PREC>::N); mbar_init(&G.tempty[i], 1); }
+        for (int i = 0; i < kTaskRing; ++i) { mbar_init(&G.qfull[i], 1); mbar_init(&G.qempty[i], TaskConsumers<PREC>::N); }
         for (int i = 0; i < kTaskRing; ++i) { mbar_init(&G.sfull[i], 1); mbar_init(&G.sempty[i], 1); }
         G.tmem_base = tmem_base;
+        G.pp_corr = 0;
+        G.pp_cph = 0;
         mbar_fence_init();
     }
     fence_proxy_async_smem();   // the smem region was written by the generic proxy in phases 1-2
     __syncthreads();
     // Role placement follows the warp arbiter (highest warp id first): the single-lane MMA issuer
     // and TMA producer get the top warp ids so busy converter/epilogue warps cannot starve them.
-    if (warp == kWarpMma) {
-        if ((tid & 31) == 0) gemm_mma<PREC>(P, ring, G, trace, (cta == 0 && R.chunklog) ? R.chunklog : nullptr);
+    if (warp == kWarpMma || (PREC == kFP32 && warp == kWarpTmem)) {
+        unsigned long long* clog = (cta == 0 && R.chunklog) ? R.chunklog : nullptr;
+        if constexpr (PREC == kFP32) gemm_mma_fp32_pp(P, ring, G, trace, clog, warp == kWarpMma ? 0 : 1);
+        else gemm_mma<PREC>(P, ring, G, trace, clog);
     } else if (warp == kWarpProducer) {
         if ((tid & 31) == 0) gemm_producer<PREC>(P, R, ring, G, trace);
     } else if (warp >= kWarpConv0 && warp < kWarpConv0 + 4) {
@@ -2658,7 +2900,7 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
     __syncthreads();
     // sequential schedule: every rank's expert compute drains before any combine starts
     if (P.sequential && !group_barrier(P, R, P.launch_seq + 4, 1, cta)) goto done;
-    if (tid == 0) trace[4] = globaltimer();
+    if (tid == 0) { trace[4] = globaltimer(); trace[kTrClkFfn1] = clock64(); }
 
     // phase 4: combine (fused into the GEMM1 epilogues when P.fused_combine)
     if (!P.fused_combine && ld_volatile_u32(P.abort_flag) == 0) combine_phase(P, R, O, smem, s_n_expert, s_stat);
@@ -2668,6 +2910,7 @@ done:
     __syncthreads();
     if (tid == 0) {
         trace[6] = globaltimer();
+        trace[kTrClkEnd] = clock64();
         trace[7] = s_stat[0] + s_stat[1];
         emit_event(P, R, kEvSpawn, cta, 0, trace[0], trace[6], R.rank, -1, -1, -1, -1, 0);
     }
@@ -2768,7 +3011,7 @@ __global__ void __launch_bounds__(kThreads, 1) debug_gemm_kernel(const __grid_co
                                 kb * Cfg::BK + at * Cfg::ATOM_K, 0);
             if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
         }
-    } else if (tid == kWarpMma * 32) {
+    } else if (warp == kWarpMma) {   // the whole warp, one elected lane issues (as in the layer kernel)
         if constexpr (PREC == kFP32) {
             LaunchParams P{};
             P.abort_flag = abort_flag;
@@ -2778,16 +3021,17 @@ __global__ void __launch_bounds__(kThreads, 1) debug_gemm_kernel(const __grid_co
         } else {
             int stage = 0; uint32_t phase = 0;
             for (int kb = 0; kb < nk; ++kb) {
-                mbar_wait(&G.ready[stage], phase, abort_flag);
+                wwait(&G.ready[stage], phase, abort_flag);
                 tc_fence_after();
-                issue_stage<PREC, 0, StageMmas<PREC>::N>(tmem, tmem + Cfg::TMEM_A0 + stage * Cfg::A_COLS,
-                                                         umma_desc_kmajor(smem_u32(smem + stage * Cfg::STAGE_BYTES), 128),
-                                                         kb == 0);
-                mma_commit(&G.done[stage]);
+                const uint64_t bd = umma_desc_kmajor(smem_u32(smem + stage * Cfg::STAGE_BYTES), 128);
+                if (elect_one())
+                    issue_stage<PREC, 0, StageMmas<PREC>::N>(tmem, tmem + Cfg::TMEM_A0 + stage * Cfg::A_COLS, bd, kb == 0);
+                __syncwarp();
+                wcommit(&G.done[stage]);
                 if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
             }
         }
-        mma_commit(&G.tfull[0]);
+        wcommit(&G.tfull[0]);
     } else if (warp >= kWarpConv0 && warp < kWarpConv0 + 4) {
         LaunchParams P{};
         P.H = K; P.D = K; P.abort_flag = abort_flag;
@@ -2816,6 +3060,52 @@ template <int KIND, int N>
 __device__ __forceinline__ void mma_burst(uint32_t d, uint32_t a_t, uint64_t b, int iters, int walk) {
     constexpr uint32_t idesc = umma_idesc(KIND == 0 ? 2u : 1u, 128, N);
     mma_tf32_ts(d, a_t, b, idesc, 0u);
+    if (walk == 4 || walk == 5) {   // streaming operands: 40 distinct B (10 atoms x 4 k-steps), A walks 32 groups
+        for (int i = 1; i < iters; i += 40) {
+#pragma unroll
+            for (int j = 0; j < 40; ++j) {
+                const uint32_t aa = walk == 4 ? a_t + (uint32_t)((j % 32) * 8) : a_t + (uint32_t)((j & 3) * 8);
+                mma_tf32_ts(d, aa, b + (uint64_t)((((j >> 2) % 10) * 16384 + (j & 3) * 32) >> 4), idesc, 1u);
+            }
+        }
+        return;
+    }
+    if (walk == 6) {   // B streams (40 distinct), A fixed 4 groups -- see walk 5; walk 7: A streams, B 8 fixed
+        for (int i = 1; i < iters; i += 40) {
+#pragma unroll
+            for (int j = 0; j < 40; ++j)
+                mma_tf32_ts(d, a_t + (uint32_t)((j % 32) * 8), b + (uint64_t)((((j >> 2) & 1) * 16384 + (j & 3) * 32) >> 4), idesc, 1u);
+        }
+        return;
+    }
+    if (walk == 7) {   // the FFN pattern with the A slot (TMEM +64 columns) and B atom (+16 KB) alternating per group
+        for (int i = 1; i < iters; i += 24) {
+#pragma unroll
+            for (int sl = 0; sl < 2; ++sl) {
+                const uint32_t a = a_t + 128u + sl * 64u;
+                const uint64_t bd = b + (uint64_t)(sl * 1024);
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) mma_tf32_ts(d, a + 32 + ks * 8, bd + ((ks * 32) >> 4), idesc, 1u);
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) mma_tf32_ts(d, a + ks * 8, bd + ((32768 + ks * 32) >> 4), idesc, 1u);
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) mma_tf32_ts(d, a + ks * 8, bd + ((ks * 32) >> 4), idesc, 1u);
+            }
+        }
+        return;
+    }
+    if (walk >= 2) {   // the FFN's 12-MMA half-stage pattern (lo*hi, hi*lo from plane +32 KB, hi*hi)
+        const uint32_t a = a_t + (walk == 3 ? 128u : 0u);   // walk 3: A at column 384 (the kernel's ring)
+        for (int i = 1; i < iters; i += 12) {
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) mma_tf32_ts(d, a + 32 + ks * 8, b + ((ks * 32) >> 4), idesc, 1u);
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) mma_tf32_ts(d, a + ks * 8, b + ((32768 + ks * 32) >> 4), idesc, 1u);
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) mma_tf32_ts(d, a + ks * 8, b + ((ks * 32) >> 4), idesc, 1u);
+        }
+        return;
+    }
     for (int i = 1; i < iters; i += 8) {
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
@@ -2910,6 +3200,223 @@ __global__ void __launch_bounds__(384, 1) debug_mma_rate_kernel(int kind, int N,
         s_stop = 1;
     }
     __syncthreads();
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) { tc_fence_after(); tmem_dealloc(tmem, 512); }
+}
+
+template <int VAR>
+__device__ __forceinline__ void issue12_var(uint32_t d, uint32_t a, uint64_t bd, uint32_t idesc, uint32_t acc) {
+#pragma unroll
+    for (int i = 0; i < 12; ++i) {
+        const int ks = i & 3, p = i >> 2;
+        uint32_t ao; uint32_t bo;
+        if (VAR == 1) { ao = (p == 0 ? 32 : 0) + ks * 8; bo = ks * 32; }                          // B plane 0 only
+        else if (VAR == 2) { ao = ks * 8; bo = (p == 1 ? 32768 : 0) + ks * 32; }                // A hi only
+        else if (VAR == 3) { ao = ks * 8; bo = ks * 32; }                                        // same 4 (A, B) x3
+        else if (VAR == 4) { ao = (i & 7) * 8; bo = (i & 7) * 32; }                              // 8 distinct
+        else if (VAR == 5) { ao = (p == 1 ? 32 : 0) + ks * 8; bo = (p == 2 ? 32768 : 0) + ks * 32; }   // hi.hi, lo.hi, hi.lo
+        else if (VAR == 6) { ao = (p == 0 ? 32 : 0) + ks * 8; bo = (p == 1 ? 16384 : 0) + ks * 32; }   // plane 1 at +16 KB
+        else { ao = (p == 0 ? 32 : 0) + ks * 8; bo = (p == 1 ? 32768 : 0) + ks * 32; }          // = the FFN's order
+        mma_tf32_ts(d, a + ao, bd + (bo >> 4), idesc, i ? 1u : acc);
+    }
+}
+
+// FFN pipeline skeleton microbenchmark (148 CTAs x 384 threads): the MMA warp's 3xTF32 issue pattern
+// with the layer's barrier protocol, without memory traffic. mode bits: 1 = FFN accumulator pattern
+// (lo*hi, hi*lo -> correction accumulator, hi*hi -> main) else every MMA into one accumulator;
+// 2 = 2-slot TMEM A ring handshake with 4 converter warps (aempty -> afull); 4 = converters tcgen05.st the
+// hi/lo half-stage (64 columns) each time; 8 = per-stage token ring handshake with a producer lane
+// (done -> ready, 2 slots). N = MMA N (128 or 256; 256 implies one accumulator). nhalf half-stages of
+// 12 MMAs (M=128, K=8 each). Writes cycles of CTA i to out[i].
+__global__ void __launch_bounds__(384, 1) debug_pipe_kernel(int mode, int N, int nhalf, unsigned long long* out) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    __shared__ uint32_t s_tmem;
+    __shared__ __align__(8) uint64_t afull[2], aempty[2], ready[2], done[2], fin;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x)
+        reinterpret_cast<float*>(smem)[i] = (float)((i * 2654435761u) >> 20) * 1e-3f - 2.0f;
+    if (warp == 0) { tmem_alloc(&s_tmem, 512); tmem_relinquish(); }
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&afull[i], 4); mbar_init(&aempty[i], 1); mbar_init(&ready[i], 1);
+            mbar_init(&done[i], (mode & 4096) ? 2 : 1);
+        }
+        mbar_init(&fin, (mode & 4096) ? 2 : 1);
+        mbar_fence_init();
+    }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = s_tmem;
+    const uint64_t bdesc = umma_desc_kmajor(smem_u32(smem), 128);
+    const long long t0 = clock64();
+    if ((mode & 1024) && warp < 4) {   // bit 1024: valid tf32 data in the A ring (columns 256..511)
+        uint32_t v[16];
+        for (int i = 0; i < 16; ++i) v[i] = __float_as_uint((float)((threadIdx.x * 16 + i) % 7) * 0.25f - 0.7f);
+        for (int c = 0; c < 256; c += 16) tmem_st16(tmem + ((uint32_t)(warp * 32) << 16) + 256 + c, v);
+        tmem_wait_st();
+        tc_fence_before();
+    }
+    __syncthreads();
+    tc_fence_after();
+    const int issuer = (mode & 256) ? 0 : 11;   // bit 256: issue from warp 0 (free-running modes only)
+    const bool pingpong = (mode & 4096) != 0;   // bit 4096: warps 11 / 9 issue alternate half-stages (named-barrier hand-off)
+    if ((mode & (2048 | 4096)) && (warp == issuer || (pingpong && warp == 9))) {
+        const uint32_t idesc = umma_idesc(2u, 128, (uint32_t)N);
+        const uint32_t d_main = tmem, d_corr = tmem + 256u;
+        uint32_t aph[2] = {0, 0}, rph[2] = {0, 0};
+        const int par = pingpong ? (warp == 9 ? 1 : 0) : -1;
+        for (int h = 0; h < nhalf; ++h) {
+            const int sl = h & 1, st = (h >> 1) & 1;
+            const bool mine = par < 0 || sl == par;
+            if ((mode & 8) && sl == 0) {   // both issuers track the token stage (each reads one of its atoms)
+                if (par < 0 || true) {
+                    while (!mbar_try_wait(&ready[st], rph[st])) {}
+                    rph[st] ^= 1u;
+                }
+            }
+            if (!mine) continue;
+            if (mode & 2) {
+                while (!mbar_try_wait(&afull[sl], aph[sl])) {}
+                aph[sl] ^= 1u;
+            }
+            tc_fence_after();
+            if (pingpong && h > 0) asm volatile("bar.sync %0, 64;" ::"r"(1 + par) : "memory");   // h-1 issued
+            const uint32_t a = tmem + 384u + (uint32_t)sl * 64u;
+            const uint64_t bd = bdesc + (uint64_t)(sl * 1024);
+            if (elect_one()) {
+                if (mode & 1) {
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks) mma_tf32_ts(d_corr, a + 32 + ks * 8, bd + ((ks * 32) >> 4), idesc, (h | ks) ? 1u : 0u);
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks) mma_tf32_ts(d_corr, a + ks * 8, bd + ((32768 + ks * 32) >> 4), idesc, 1u);
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks) mma_tf32_ts(d_main, a + ks * 8, bd + ((ks * 32) >> 4), idesc, (h | ks) ? 1u : 0u);
+                } else {
+                    issue12_var<7>(d_main, a, bd, idesc, h ? 1u : 0u);
+                }
+                if (mode & 2) mma_commit(&aempty[sl]);
+                if (mode & 8) { if (pingpong || sl == 1) mma_commit(&done[st]); }
+            }
+            __syncwarp();
+            if (pingpong && h + 1 < nhalf) asm volatile("bar.arrive %0, 64;" ::"r"(2 - par) : "memory");   // h issued
+        }
+        if (elect_one()) mma_commit(&fin);
+        __syncwarp();
+        if (warp == issuer) {
+            while (!mbar_try_wait(&fin, 0)) {}
+            if (lane == 0) out[blockIdx.x] = (unsigned long long)(clock64() - t0);
+        }
+    }
+    if ((mode & (2048 | 4096)) && (warp == issuer || (pingpong && warp == 9))) nhalf = 0;
+    if (warp == issuer && lane == 0) {
+        const uint32_t idesc = umma_idesc(2u, 128, (uint32_t)N);
+        const uint32_t d_main = tmem, d_corr = tmem + 256u;   // (N = 256: one accumulator at column 0)
+        uint32_t aph[2] = {0, 0}, rph[2] = {0, 0};
+        if (mode == 240) {   // var 15: branch-free loop, h unrolled x2 (compile-time slot), FFN order, one acc
+            for (int h = 0; h < nhalf; h += 2) {
+#pragma unroll
+                for (int sl = 0; sl < 2; ++sl)
+                    issue12_var<7>(d_main, tmem + 384u + sl * 64u, bdesc + (uint64_t)(sl * 1024), idesc, h + sl ? 1u : 0u);
+            }
+            mma_commit(&fin);
+            while (!mbar_try_wait(&fin, 0)) {}
+            out[blockIdx.x] = (unsigned long long)(clock64() - t0);
+            nhalf = 0;
+        }
+        for (int h = 0; h < nhalf; ++h) {
+            const int sl = h & 1, st = (h >> 1) & 1;
+            if ((mode & 8) && sl == 0) {
+                while (!mbar_try_wait(&ready[st], rph[st])) {}
+                rph[st] ^= 1u;
+                tc_fence_after();
+            }
+            if (mode & 2) {
+                while (!mbar_try_wait(&afull[sl], aph[sl])) {}
+                aph[sl] ^= 1u;
+                tc_fence_after();
+            }
+            const int var = (mode >> 4) & 15;
+            // var 8/9/10: FFN order into one accumulator with the A ring at TMEM column 256 / 128 / 320
+            const uint32_t a_base = (var == 8 || var == 11) ? 256u : var == 9 ? 128u : var == 10 ? 320u : 384u;
+            const uint32_t a = tmem + a_base + (uint32_t)sl * (var == 10 ? 96u : 64u);
+            const uint64_t bd = bdesc + (uint64_t)(sl * 1024);   // the stage's second 128-byte atom
+            const uint32_t acc = h == 0 ? 0u : 1u;
+            if (var) {   // free-running pattern variants (one accumulator, compile-time operand offsets)
+                switch (var) {
+                    case 1: issue12_var<1>(d_main, a, bd, idesc, acc); break;
+                    case 2: issue12_var<2>(d_main, a, bd, idesc, acc); break;
+                    case 3: issue12_var<3>(d_main, a, bd, idesc, acc); break;
+                    case 4: issue12_var<4>(d_main, a, bd, idesc, acc); break;
+                    case 5: issue12_var<5>(d_main, a, bd, idesc, acc); break;
+                    case 6: issue12_var<6>(d_main, a, bd, idesc, acc); break;
+                    case 9: issue12_var<7>(var == 9 ? tmem + 256u : d_main, a, bd, idesc, acc); break;
+                    case 11: {   // FFN accumulator pattern with the A ring at 256: corrections into column 384
+                        const uint32_t dc = tmem + 384u;
+#pragma unroll
+                        for (int ks = 0; ks < 4; ++ks) mma_tf32_ts(dc, a + 32 + ks * 8, bd + ((ks * 32) >> 4), idesc, ks ? 1u : acc);
+#pragma unroll
+                        for (int ks = 0; ks < 4; ++ks) mma_tf32_ts(dc, a + ks * 8, bd + ((32768 + ks * 32) >> 4), idesc, 1u);
+#pragma unroll
+                        for (int ks = 0; ks < 4; ++ks) mma_tf32_ts(d_main, a + ks * 8, bd + ((ks * 32) >> 4), idesc, ks ? 1u : acc);
+                        break;
+                    }
+                    default: issue12_var<7>(d_main, a, bd, idesc, acc); break;
+                }
+            } else if ((mode & 1) && N <= 128) {
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) mma_tf32_ts(d_corr, a + 32 + ks * 8, bd + ((ks * 32) >> 4), idesc, ks ? 1u : acc);
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) mma_tf32_ts(d_corr, a + ks * 8, bd + ((32768 + ks * 32) >> 4), idesc, 1u);
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) mma_tf32_ts(d_main, a + ks * 8, bd + ((ks * 32) >> 4), idesc, ks ? 1u : acc);
+            } else {
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) mma_tf32_ts(d_main, a + 32 + ks * 8, bd + ((ks * 32) >> 4), idesc, ks ? 1u : acc);
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) mma_tf32_ts(d_main, a + ks * 8, bd + ((32768 + ks * 32) >> 4), idesc, 1u);
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) mma_tf32_ts(d_main, a + ks * 8, bd + ((ks * 32) >> 4), idesc, 1u);
+            }
+            if (mode & 2) mma_commit(&aempty[sl]);
+            if ((mode & 8) && sl == 1) mma_commit(&done[st]);
+        }
+        if (mode != 240 && !(mode & (2048 | 4096))) {
+            mma_commit(&fin);
+            while (!mbar_try_wait(&fin, 0)) {}
+            out[blockIdx.x] = (unsigned long long)(clock64() - t0);
+        }
+    } else if (warp < 4 && (mode & 2)) {
+        uint32_t eph[2] = {1, 1};
+        uint32_t v[16];
+        for (int i = 0; i < 16; ++i) v[i] = __float_as_uint((float)((threadIdx.x * 16 + i) % 7) * 0.25f - 0.7f);
+        const uint32_t lane_addr = (uint32_t)(warp * 32) << 16;
+        for (int h = 0; h < nhalf; ++h) {
+            const int sl = h & 1;
+            while (!mbar_try_wait(&aempty[sl], eph[sl])) {}
+            eph[sl] ^= 1u;
+            tc_fence_after();
+            if (mode & 4) {
+                const uint32_t col = tmem + lane_addr + 384u + (uint32_t)sl * 64u;
+                tmem_st16(col, v); tmem_st16(col + 16, v); tmem_st16(col + 32, v); tmem_st16(col + 48, v);
+                tmem_wait_st();
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&afull[sl]);
+        }
+    } else if (warp == 10 && lane == 0 && (mode & 8)) {
+        uint32_t dph[2] = {1, 1};
+        for (int s = 0; s < (nhalf + 1) / 2; ++s) {
+            const int st = s & 1;
+            while (!mbar_try_wait(&done[st], dph[st])) {}
+            dph[st] ^= 1u;
+            mbar_arrive(&ready[st]);
+        }
+    }
     tc_fence_before();
     __syncthreads();
     if (warp == 0) { tc_fence_after(); tmem_dealloc(tmem, 512); }
@@ -3061,8 +3568,13 @@ cudaError_t launch_debug_latency(int n, unsigned long long* out) {
 }
 
 cudaError_t launch_debug_mma_rate(int kind, int N, int iters, int nissuers, unsigned long long* out) {
+    if (kind >= 16) {   // pipeline skeleton: kind = 16 + mode, iters = half-stages
+        cudaFuncSetAttribute(debug_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024);
+        debug_pipe_kernel<<<148, ((kind - 16) & 512) ? 128 : 384, 66 * 1024>>>(kind - 16, N, iters, out);
+        return cudaGetLastError();
+    }
     cudaFuncSetAttribute(debug_mma_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 161 * 1024);
-    const int walk = (nissuers >> 4) & 1;
+    const int walk = (nissuers >> 4) & 7;
     const int grid = (nissuers >> 8) & 255 ? (nissuers >> 8) & 255 : 1;   // number of SMs running the benchmark
     const int spin_mode = (nissuers >> 16) & 7;
     const int threads = spin_mode ? 384 : 128;                             // + 8 noise warps

@@ -150,6 +150,7 @@ struct Group {
     int num_sms = 0;
     unsigned long long launch_seq = 0;
     uint32_t zero_seq = 0;          // fused-combine launches since the control block was cleared
+    cudaStream_t last_stream = nullptr;   // stream of the previous launch (cross-stream ordering)
 };
 
 // control block offsets
@@ -585,6 +586,17 @@ static fdmoe_status launch_all(fdmoe_handle* h, const float* const* in_dev, floa
         fdmoe_status ds = fdmoe_straggler_delays(opts, d.P, d.El, delay.data());
         if (ds) return ds;
     }
+    // The kernel reads the input shards while other CTAs already write outputs (the fused combine zeroes
+    // and accumulates output rows during the FFN; the separate combine writes them while late packets may
+    // still be in flight from peers): in-place forwards are not supported.
+    for (auto& g : h->groups)
+        for (int idx : g.members) {
+            const uint8_t* a = reinterpret_cast<const uint8_t*>(in_dev[idx]);
+            const uint8_t* o = reinterpret_cast<const uint8_t*>(out_dev[idx]);
+            const size_t bytes = (size_t)d.S * d.H * 4;
+            if (!a || !o) return fail(FDMOE_ERR_CONFIG, "null shard pointer");
+            if (a < o + bytes && o < a + bytes) return fail(FDMOE_ERR_CONFIG, "input and output shards overlap");
+        }
     h->epoch += 1;
     for (auto& g : h->groups) {
         LaunchParams p{};
@@ -649,6 +661,11 @@ static fdmoe_status launch_all(fdmoe_handle* h, const float* const* in_dev, floa
         CK(cudaSetDevice(g.dev));
         cudaStream_t s = g.stream;
         if (streams && streams[g.members[0]]) s = static_cast<cudaStream_t>(streams[g.members[0]]);
+        // Launches share the control block, heaps and C1 of the handle: a launch on another stream than the
+        // previous one is ordered behind it (ev1 = end of the previous launch, whatever stream it ran on;
+        // a no-op for back-to-back launches on one stream).
+        if (h->in_flight && s != g.last_stream) CK(cudaStreamWaitEvent(s, g.ev1, 0));
+        g.last_stream = s;
         for (int idx : g.members) {
             RankRes& r = h->ranks[idx];
             if (trace_events) CK(cudaMemsetAsync(r.ctrl + ctrl_ev_ctr(d), 0, 4, s));
@@ -758,10 +775,16 @@ fdmoe_status fdmoe_forward(fdmoe_handle* h, const float* const* in_shards, float
             so.gemm1 = (int64_t)(s1[1] - stat0[i * 8 + 1]);
             so.combine = (int64_t)(s1[2] - stat0[i * 8 + 2]);
             so.executed = so.gemm0 + so.gemm1 + so.combine;
-            so.enqueued = so.executed;
-            so.scheduled_final = so.executed;
-            so.bound_final = so.executed;
-            so.bound_initial = d.El * d.MT * (d.NB0 + d.NB1) + (d.S + kCombineTok - 1) / kCombineTok;
+            // device task accounting (fdmoe_kernel.cu gemm_producer): bound self-corrected per resolved row
+            // tile, scheduled = non-empty FFN tasks the producers handed to their pipelines; the combine tasks
+            // of the separate phase are static (the fused combine has none)
+            const int64_t comb_bound = so.combine ? (d.S + kCombineTok - 1) / kCombineTok : 0;
+            const int64_t bdelta = (int64_t)(s1[5] - stat0[i * 8 + 5]);
+            so.bound_initial = d.El * d.MT * (d.NB0 + d.NB1) + comb_bound;
+            so.bound_final = so.bound_initial + bdelta;
+            so.scheduled_final = (int64_t)(s1[6] - stat0[i * 8 + 6]) + so.combine;
+            so.enqueued = so.scheduled_final;
+            so.tiles_resolved = (int64_t)(s1[7] - stat0[i * 8 + 7]);
             so.launches = 1;
             so.gate_exact_tokens = (int64_t)(s1[3] - stat0[i * 8 + 3]);
             so.gate_pair_tokens = (int64_t)(s1[4] - stat0[i * 8 + 4]);
@@ -993,7 +1016,7 @@ fdmoe_status fdmoe_debug_mma_rate(int32_t kind, int32_t nissuers, int32_t N, int
     unsigned long long c = 0;
     for (int i = 0; i < 256; ++i) c = std::max(c, cs[i]);   // slowest SM
     cudaFree(d);
-    *cycles_per_mma = (double)c / ((double)iters * (nissuers & 15));
+    *cycles_per_mma = kind >= 16 ? (double)c / ((double)iters * 12.0) : (double)c / ((double)iters * (nissuers & 15));
     return FDMOE_OK;
 }
 

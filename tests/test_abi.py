@@ -43,7 +43,7 @@ def test_product_library_has_no_diagnostics_and_dev_library_has_them():
 
 
 def test_abi_version():
-    assert fd.lib().fdmoe_abi_version() == 2
+    assert fd.lib().fdmoe_abi_version() == 3
 
 
 def test_library_is_sm100a_only():

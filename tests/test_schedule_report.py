@@ -40,7 +40,7 @@ int main() {
     O = fd._Opts
     assert got == [C.sizeof(O), O.straggler_a.offset, O.seed.offset, EVENT_DTYPE.itemsize,
                    EVENT_DTYPE.fields["value"][1]]
-    assert fd.lib().fdmoe_abi_version() == 2
+    assert fd.lib().fdmoe_abi_version() == 3
 
 
 @needs_ref

@@ -27,6 +27,10 @@ print(f"slowest gate CTA {worst}: logits {t[worst, 24]/1:.1f} pairs {t[worst, 25
       f"(full-exact tokens {int(round(t[worst, 27] * 1e3))}); median CTA: logits {np.median(t[:, 24]):.1f} "
       f"pairs {np.median(t[:, 25]):.1f} full {np.median(t[:, 26]):.1f}")
 print("ffn tiles per CTA: min", int(tr[:, 7].min()), "max", int(tr[:, 7].max()), "sum", int(tr[:, 7].sum()))
+raw = tr
+for a, b, ca, cb, n in ((0, 3, 32, 33, "start..FFN"), (3, 4, 33, 34, "FFN"), (0, 6, 32, 35, "launch")):
+    mhz = (raw[:, cb] - raw[:, ca]) / np.maximum(raw[:, b] - raw[:, a], 1) * 1e3
+    print(f"effective SM clock {n:11s}: median {np.median(mhz):7.1f} MHz (min {mhz.min():.1f}, max {mhz.max():.1f})")
 ffn_cyc = (t[:, 4] - t[:, 3]).mean() * 1e3 * 1.965   # ns -> cycles at max clock (approx)
 for i, n in enumerate(["mma<-tokens", "mma<-weights", "mma<-acc", "conv<-wTMA", "conv<-tmemA", "prod<-wslot", "prod<-xslot", "epi<-acc"]):
     print(f"wait {n:14s} mean {tr[:, 8 + i].mean() / 1e3:9.1f} kcyc  ({100 * tr[:, 8 + i].mean() / ffn_cyc:5.1f}% of FFN phase)")
