@@ -31,6 +31,7 @@ constexpr int kMaxSrcPerTile = 8;   // packet_rows >= 16 -> <= 8 packets per 128
 constexpr int kCombineTok = 16;     // tokens per combine task (== kGateTok)
 constexpr int kMaxLocalRanks = 8;   // ranks per launch (virtual ranks on one GPU)
 constexpr int kTracePts = 40;
+constexpr int kFullCap = 256;       // rank-wide full-exact token list capacity (overflow: the owner CTA computes)
 constexpr int kGroupBarriers = 2;   // sequential mode: after dispatch, after the expert FFN
 constexpr int kChunkLog = 512;       // start, gate, barrier, dispatch, gemm, combine, end, tiles,
                                     // then FFN pipeline wait cycles (see kWait*)
@@ -42,7 +43,8 @@ enum WaitSlot : int {
     kTrGateTc = 28,                                               // tensor-core gate logits done
     kTrGateLoad = 29,                                             // tensor-core logits staged for routing
     kTrGateDecide = 30, kTrGateExp = 31,                          // thread-route decisions / exps done
-    kTrClk0 = 32, kTrClkFfn0, kTrClkFfn1, kTrClkEnd               // clock64 at start / FFN start / FFN end / end
+    kTrClk0 = 32, kTrClkFfn0, kTrClkFfn1, kTrClkEnd,              // clock64 at start / FFN start / FFN end / end
+    kTrFullChains = 36, kTrFullRouted = 37                        // distributed full-exact pass: chains claimed / routed
 };
 
 enum Prec : int { kFP32 = 0, kBF16 = 1 };
@@ -110,6 +112,9 @@ struct alignas(64) RankCtx {
     DevEvent* ev;              // [ev_cap] device event log (fdmoe_event layout)
     uint32_t* ev_ctr;          // records emitted this launch (reset by the host before the launch)
     uint32_t* zero_ctr;        // fused combine: CTAs whose output rows are zeroed (monotonic)
+    uint32_t* full_ctr;        // [3] distributed full-exact pass: tokens listed, chains claimed, chains done
+    int32_t* full_list;        // [kFullCap] tokens needing every expert's exact logit (ties / near-ties)
+    float* full_z;             // [kFullCap][E_total] their exact logits (reference chain, gate.hpp:77-81)
     uint32_t ev_cap;
     int32_t rank;
 };

@@ -961,6 +961,111 @@ __device__ bool route_resolve(const LaunchParams& P, const RankCtx& R, float* ro
     return true;
 }
 
+// Distributed full-exact pass (after the gate barrier; every CTA of the rank). A near-tie token needs all E
+// reference logits: E sequential H-long chains over 2 x H*E*4 bytes of Wg that one SM streams at its own
+// memory-level parallelism (~50 us for the CTA that holds the token, the whole rank waiting at the next
+// barrier). Here each (listed token, expert) chain is one warp's item: the lanes load the token row and the
+// Wg^T row, form the products fl(a_x w_x) in parallel, and lane 0 runs the separately-rounded chain over them
+// in x order (gate.hpp:77-81) -- bit-identical to the owner's pass, ~5 us for all E chains at once. The owners
+// then route their tokens from R.full_z (route_exact). Returns false on abort.
+__device__ bool full_exact_distributed(const LaunchParams& P, const RankCtx& R, const float* __restrict__ A,
+                                       uint8_t* smem, int cta, const unsigned long long* tab) {
+    const int E = P.E, H = P.H, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int kWarps = kThreads / 32;
+    const int nf = (int)min(ld_volatile_u32(&R.full_ctr[0]), (uint32_t)kFullCap);
+    if (nf == 0) return true;
+    const int items = nf * E;
+    float* prod = reinterpret_cast<float*>(smem) + warp * 1024;   // 4 KB per warp: products of one 1024-x chunk
+    while (true) {
+        int it = 0;
+        if (lane == 0) it = (int)atomicAdd(&R.full_ctr[1], 1u);
+        it = __shfl_sync(0xffffffffu, it, 0);
+        if (it >= items) break;
+        const int t = it / E, e = it - t * E;
+        const int tok = R.full_list[t];
+        const float4* a4 = reinterpret_cast<const float4*>(A + (size_t)tok * H);
+        const float4* w4 = reinterpret_cast<const float4*>(R.wgT + (size_t)e * H);
+        float z = 0.0f;
+        for (int x0 = 0; x0 < H; x0 += 1024) {
+            const int n4 = min(1024, H - x0) / 4;   // H % 32 == 0 (envelope): whole float4 groups
+            float4 av[8], wv[8];   // every load of the chunk in flight at once (one L2 round trip per chunk)
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = lane + 32 * u;
+                if (i < n4) { av[u] = __ldcg(a4 + x0 / 4 + i); wv[u] = __ldcg(w4 + x0 / 4 + i); }
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = lane + 32 * u;
+                if (i < n4)
+                    reinterpret_cast<float4*>(prod)[i] = make_float4(__fmul_rn(av[u].x, wv[u].x), __fmul_rn(av[u].y, wv[u].y),
+                                                                     __fmul_rn(av[u].z, wv[u].z), __fmul_rn(av[u].w, wv[u].w));
+            }
+            __syncwarp();
+            if (lane == 0) {
+#pragma unroll 4
+                for (int i = 0; i < n4; ++i) {
+                    const float4 p = reinterpret_cast<const float4*>(prod)[i];
+                    z = __fadd_rn(z, p.x); z = __fadd_rn(z, p.y); z = __fadd_rn(z, p.z); z = __fadd_rn(z, p.w);
+                }
+            }
+            __syncwarp();
+        }
+        if (lane == 0) {
+            R.full_z[(size_t)t * E + e] = z;
+            __threadfence();
+            atomicAdd(&R.full_ctr[2], 1u);
+        }
+    }
+    if (tid == 0) R.trace[(size_t)cta * kTracePts + kTrFullChains] = globaltimer();
+    // owners: route their listed tokens once every chain is done; their picks join the CTA's counts
+    int* sCnt = reinterpret_cast<int*>(smem) + kWarps * 1024 + kWarps * kMaxExperts;
+    for (int e = tid; e < E; e += kThreads) sCnt[e] = 0;
+    __syncthreads();
+    int tokA, tokB, b0, b1;
+    gate_token_range(P, cta, tokA, tokB, b0, b1);
+    bool mine_any = false;
+    for (int t = warp; t < nf; t += kWarps) {
+        const int tok = R.full_list[t];
+        if (tok < tokA || tok >= tokB) continue;
+        mine_any = true;
+        int ok = 1;
+        if (lane == 0) {
+            const uint64_t t0 = globaltimer();
+            uint32_t n = 0;
+            while (ld_acquire_gpu_u32(&R.full_ctr[2]) < (uint32_t)items) {
+                if ((++n & 255u) == 0) {
+                    if (ld_volatile_u32(P.abort_flag)) { ok = 0; break; }
+                    if (globaltimer() - t0 > P.budget_ns) {
+                        raise_error(P, R, kErrTimeout, 120, (uint32_t)items, 0);
+                        ok = 0;
+                        break;
+                    }
+                }
+            }
+        }
+        if (!__shfl_sync(0xffffffffu, ok, 0)) break;
+        float* row = reinterpret_cast<float*>(smem) + kWarps * 1024 + warp * kMaxExperts;
+        for (int e = lane; e < E; e += 32) row[e] = __ldcg(R.full_z + (size_t)t * E + e);
+        __syncwarp();
+        route_exact(P, R, row, tok, sCnt, tab);
+    }
+    __shared__ int s_any, s_ok;
+    if (tid == 0) s_any = 0;
+    __syncthreads();
+    if (mine_any && lane == 0) s_any = 1;
+    __syncthreads();
+    if (s_any)
+        for (int e = tid; e < E; e += kThreads)
+            if (sCnt[e]) R.cnt_cta[(size_t)cta * E + e] += sCnt[e];
+    if (tid == 0) {
+        s_ok = ld_volatile_u32(P.abort_flag) == 0;
+        R.trace[(size_t)cta * kTracePts + kTrFullRouted] = globaltimer();
+    }
+    __syncthreads();
+    return s_ok != 0;
+}
+
 __device__ void gate_phase(const LaunchParams& P, const RankCtx& R, const float* __restrict__ A, int cta,
                            uint8_t* smem, unsigned long long* stat, const unsigned long long* tab) {
     const int E = P.E;
@@ -1104,8 +1209,19 @@ __device__ void gate_phase(const LaunchParams& P, const RankCtx& R, const float*
         if (tid == 0) R.trace[(size_t)cta * kTracePts + kTrGatePairs] = globaltimer();
         const int nf = s_nfull;
         if (nf > 0 && !(FD_DBG(kDbgGateNoFlush))) {   // ties / near-ties / overflow: the reference chain for all E
-            gate_full_exact(P, R, A, g, nf);
-            for (int t = warp; t < nf; t += kWarps) route_exact(P, R, g.sL + t * Ep, g.sFull[t], g.sCnt, g.tab);
+            // Listed rank-wide: every CTA computes a share of their chains after the gate barrier
+            // (full_exact_distributed); only a list overflow is computed here by the owner alone.
+            __shared__ int s_base;
+            if (tid == 0) s_base = (int)atomicAdd(&R.full_ctr[0], (uint32_t)nf);
+            __syncthreads();
+            const int base = s_base;
+            if (base + nf <= kFullCap) {
+                for (int t = tid; t < nf; t += kThreads) R.full_list[base + t] = g.sFull[t];
+            } else {
+                if (tid == 0) atomicSub(&R.full_ctr[0], (uint32_t)nf);
+                gate_full_exact(P, R, A, g, nf);
+                for (int t = warp; t < nf; t += kWarps) route_exact(P, R, g.sL + t * Ep, g.sFull[t], g.sCnt, g.tab);
+            }
             n_full += nf;
         }
         __syncthreads();
@@ -1141,20 +1257,35 @@ __device__ void dispatch_phase(const LaunchParams& P, const RankCtx& R, const fl
         }
     };
 
+    // Per-expert prefix of the per-CTA pick counts: (expert, CTA-range part) per thread so every thread of the
+    // CTA has loads in flight (16 at a time): a thread per expert walking all 148 CTAs paid ~19 L2 round trips.
+    const int parts = E <= kThreads ? min(8, kThreads / E) : 1;
+    int* sPb = sRun + 2 * kMaxExperts;        // [parts][E] partial base (CTAs < cta) and total
+    int* sPt = sPb + 8 * kMaxExperts;
+    {
+        const int per = (P.ctas_per_rank + parts - 1) / parts;
+        for (int i = tid; i < parts * E; i += kThreads) {
+            const int e = i % E, part = i / E;
+            const int c_lo = part * per, c_hi = min(P.ctas_per_rank, c_lo + per);
+            int base = 0, tot = 0;
+            for (int c0 = c_lo; c0 < c_hi; c0 += 16) {
+                int v[16];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) v[u] = c0 + u < c_hi ? __ldcg(R.cnt_cta + (size_t)(c0 + u) * E + e) : 0;
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    if (c0 + u < cta) base += v[u];
+                    tot += v[u];
+                }
+            }
+            sPb[part * E + e] = base;
+            sPt[part * E + e] = tot;
+        }
+    }
+    __syncthreads();
     for (int e = tid; e < E; e += kThreads) {
         int base = 0, tot = 0;
-        // per-CTA pick counts of expert e (coalesced across threads); 8 loads in flight per batch —
-        // a plain loop pays one L2 round trip per CTA (148 in a row: ~40 us)
-        for (int c0 = 0; c0 < P.ctas_per_rank; c0 += 8) {
-            int v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = c0 + u < P.ctas_per_rank ? __ldcg(R.cnt_cta + (size_t)(c0 + u) * E + e) : 0;
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                if (c0 + u < cta) base += v[u];
-                tot += v[u];
-            }
-        }
+        for (int part = 0; part < parts; ++part) { base += sPb[part * E + e]; tot += sPt[part * E + e]; }
         const int n = min(tot, C);
         sRun[e] = base;
         sN[e] = n;
@@ -2841,19 +2972,23 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
         emit_event(P, R, kEvGateDone, cta, 0, trace[0], trace[1], R.rank, -1, -1, -1, -1, 0);
     }
     if (!rank_barrier(P, R, P.launch_seq)) goto done;
+    // near-tie tokens listed by the gate: every CTA computes a share of their exact chains, owners route them
+    if (!full_exact_distributed(P, R, A, smem, cta, s_exp_tab)) goto done;
+    if (!rank_barrier(P, R, P.launch_seq + 1)) goto done;
+    if (cta == 0 && tid == 0) { R.full_ctr[0] = 0; R.full_ctr[1] = 0; R.full_ctr[2] = 0; }   // next launch's list
     if (tid == 0) trace[2] = globaltimer();
 
     // phase 2: slot assignment, then (after the slot table is complete) the balanced row push
     dispatch_phase(P, R, A, cta, smem);
     if (tid == 0) trace[kTrSlots] = globaltimer();
-    if (!rank_barrier(P, R, P.launch_seq + 1)) goto done;
+    if (!rank_barrier(P, R, P.launch_seq + 2)) goto done;
     if (tid == 0) trace[kTrSlotBarrier] = globaltimer();
     push_phase(P, R, A, cta, smem);
     __syncthreads();
     if (tid == 0) trace[kTrPush] = globaltimer();
     for (int e = tid; e < P.E; e += kThreads) s_n_expert[e] = reinterpret_cast<const int*>(smem)[kMaxExperts + e];
     // sequential schedule: every rank's dispatch lands before any expert tile starts
-    if (P.sequential && !group_barrier(P, R, P.launch_seq + 2, 0, cta)) goto done;
+    if (P.sequential && !group_barrier(P, R, P.launch_seq + 3, 0, cta)) goto done;
     if (tid == 0) { trace[3] = globaltimer(); trace[kTrClkFfn0] = clock64(); }
 
     // phase 3: expert FFN tiles
@@ -2899,7 +3034,7 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
     }
     __syncthreads();
     // sequential schedule: every rank's expert compute drains before any combine starts
-    if (P.sequential && !group_barrier(P, R, P.launch_seq + 4, 1, cta)) goto done;
+    if (P.sequential && !group_barrier(P, R, P.launch_seq + 5, 1, cta)) goto done;
     if (tid == 0) { trace[4] = globaltimer(); trace[kTrClkFfn1] = clock64(); }
 
     // phase 4: combine (fused into the GEMM1 epilogues when P.fused_combine)

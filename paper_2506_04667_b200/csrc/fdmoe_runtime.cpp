@@ -123,6 +123,8 @@ struct RankRes {
     unsigned long long* chunklog = nullptr;
     unsigned long long* delay_ns = nullptr;
     DevEvent* ev = nullptr;
+    int32_t* full_list = nullptr;
+    float* full_z = nullptr;
     uint32_t ev_cap = 0;
     int ctas = 0;
     uint8_t* ctrl = nullptr;        // bar | heads | err | stats | sent | g0done
@@ -236,6 +238,8 @@ fdmoe_status alloc_rank(fdmoe_handle* h, RankRes& r, int ctas_per_rank) {
     r.ev_cap = event_capacity(d, ctas_per_rank);
     parts.push_back({(void**)&r.ev, (size_t)r.ev_cap * sizeof(DevEvent)});
     parts.push_back({(void**)&r.blk_ready, (size_t)(d.S + kGateTok - 1) / kGateTok * 4});
+    parts.push_back({(void**)&r.full_list, (size_t)kFullCap * 4});
+    parts.push_back({(void**)&r.full_z, (size_t)kFullCap * d.E * 4});
     parts.push_back({(void**)&r.ctrl, ctrl_bytes(d)});
     parts.push_back({(void**)&r.in_buf, (size_t)d.S * d.H * 4});
     parts.push_back({(void**)&r.out_buf, (size_t)d.S * d.H * 4});
@@ -300,6 +304,9 @@ fdmoe_status build_ctx(fdmoe_handle* h) {
             c.ev_cap = r.ev_cap;
             c.ev_ctr = reinterpret_cast<uint32_t*>(r.ctrl + ctrl_ev_ctr(d));
             c.zero_ctr = reinterpret_cast<uint32_t*>(r.ctrl + ctrl_ev_ctr(d) + 4);
+            c.full_ctr = reinterpret_cast<uint32_t*>(r.ctrl + ctrl_ev_ctr(d) + 8);   // [3], inside the 64 spare bytes
+            c.full_list = r.full_list;
+            c.full_z = r.full_z;
             c.bar = reinterpret_cast<unsigned long long*>(r.ctrl + kCtrlBar);
             c.gemm_head = reinterpret_cast<uint32_t*>(r.ctrl + kCtrlGemm);
             c.comb_head = reinterpret_cast<uint32_t*>(r.ctrl + kCtrlComb);
@@ -675,7 +682,7 @@ static fdmoe_status launch_all(fdmoe_handle* h, const float* const* in_dev, floa
         CK(cudaEventRecord(g.ev0, s));
         CK(launch_layer(p, g.ctas_per_rank * (int)g.members.size(), g.smem, s));
         CK(cudaEventRecord(g.ev1, s));
-        g.launch_seq += sequential ? 2 + 2 * kGroupBarriers : 2;   // rank-barrier generations used
+        g.launch_seq += sequential ? 3 + 2 * kGroupBarriers : 3;   // rank-barrier generations used
     }
     h->in_flight = true;
     return FDMOE_OK;

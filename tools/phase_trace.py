@@ -19,7 +19,7 @@ names = ["start", "gate", "barrier", "dispatch", "ffn", "combine", "end"]
 print("kernel ms", op.last_kernel_ms())
 for i, n in enumerate(names):
     print(f"{n:9s} min {t[:, i].min():9.1f}  med {np.median(t[:, i]):9.1f}  max {t[:, i].max():9.1f} us")
-for i, n in ((28, "gate-tc-logits"), (29, "gate-load"), (30, "gate-decide"), (31, "gate-exp"), (24, "gate-route"), (25, "gate-pairs"), (26, "gate-full"), (20, "prefix"), (21, "slots"), (22, "slot-barrier"), (23, "push")):
+for i, n in ((28, "gate-tc-logits"), (29, "gate-load"), (30, "gate-decide"), (31, "gate-exp"), (24, "gate-route"), (25, "gate-pairs"), (26, "gate-full"), (36, "full-chains"), (37, "full-routed"), (20, "prefix"), (21, "slots"), (22, "slot-barrier"), (23, "push")):
     print(f"{n:12s} min {t[:, i].min():9.1f}  med {np.median(t[:, i]):9.1f}  max {t[:, i].max():9.1f} us")
 g = t[:, 1]
 worst = int(np.argmax(g))
