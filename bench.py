@@ -292,6 +292,17 @@ def main():
         barrier()
     op.sync()
     ms = ev0.elapsed_time(ev1) / args.steps
+    # in-kernel SM clock of the last timed launch: per-CTA clock64 / %globaltimer deltas (device trace
+    # points kTrClk*; NVML's SM-clock reading does not show the power-cap throttling inside a launch)
+    kclk = None
+    try:
+        tr = op.trace(0).astype(np.float64)
+        f_launch = (tr[:, 35] - tr[:, 32]) / np.maximum(tr[:, 6] - tr[:, 0], 1.0) * 1e3
+        f_ffn = (tr[:, 34] - tr[:, 33]) / np.maximum(tr[:, 4] - tr[:, 3], 1.0) * 1e3
+        kclk = {"launch_mhz": round(float(np.median(f_launch)), 1), "ffn_mhz": round(float(np.median(f_ffn)), 1),
+                "source": "median over CTAs of clock64 / %globaltimer deltas, last timed launch (device trace)"}
+    except Exception as ex:  # noqa: BLE001
+        kclk = {"unavailable": str(ex)}
     if world > 1:
         ms = fdist.max_over_ranks(ms, device="cuda")
     tokens_per_step = cfg.tokens_per_device * n
@@ -379,14 +390,20 @@ def main():
     ffn_flops = 4.0 * H * D * rows
     flops = gate_flops + ffn_flops
     weight_bytes = El * 2.0 * H * D * 4   # FP32 weights read once (algorithmic)
+    # The timed region is a loop of back-to-back launches that runs at the 1 kW power cap (in-kernel SM clock
+    # ~1.4-1.5 GHz in the FFN, `clocks.in_kernel`), so the tensor peak is the driver's SUSTAINED cuBLAS figure
+    # (measured at ~1.34 GHz under the same cap; B200_PROFILING.md: "the sustained one for a kernel timed inside
+    # a long step"); the burst-peak fraction is reported beside it.
+    sus = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
     if prec == fd.Precision.fp32:
-        tensor_peak = pk["bf16_tflops"] / 2.0 / 3.0   # tf32 = bf16/2; FP32-accurate = 3 tf32 products
-        peak_note = (f"3xTF32 effective = measured bf16 {pk['bf16_tflops']:.1f} / 2 (tf32 rate) / 3 (products); "
-                     f"{pk['source']}")
+        tensor_peak = sus / 2.0 / 3.0   # tf32 = bf16/2; FP32-accurate = 3 tf32 products
+        tensor_burst = pk["bf16_tflops"] / 2.0 / 3.0
+        peak_note = (f"3xTF32 effective = measured bf16 sustained {sus:.1f} / 2 (tf32 rate) / 3 (products); burst "
+                     f"{pk['bf16_tflops']:.1f} / 6 = {tensor_burst:.1f} in peak_burst; {pk['source']}")
     else:
-        tensor_peak = pk["bf16_tflops"]
+        tensor_peak, tensor_burst = sus, pk["bf16_tflops"]
         weight_bytes /= 2
-        peak_note = f"bf16 {pk['source']}"
+        peak_note = f"bf16 sustained {sus:.1f} (burst {pk['bf16_tflops']:.1f}); HBM copy {pk['hbm_gbs']:.1f}; {pk['source']}"
     t_tensor = flops / (tensor_peak * 1e12)
     t_hbm = weight_bytes / (pk["hbm_gbs"] * 1e9)
     bound = "tensor" if t_tensor >= t_hbm else "hbm"
@@ -394,7 +411,7 @@ def main():
     achieved_gbs = weight_bytes / (ms * 1e-3) / 1e9
     if bound == "tensor":
         roof = {"bound": "tensor", "achieved": achieved_tf, "peak": tensor_peak, "unit": "TFLOP/s",
-                "frac": achieved_tf / tensor_peak}
+                "frac": achieved_tf / tensor_peak, "peak_burst": tensor_burst, "frac_burst": achieved_tf / tensor_burst}
     else:
         roof = {"bound": "hbm", "achieved": achieved_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved_gbs / pk["hbm_gbs"]}
@@ -416,7 +433,7 @@ def main():
             "vs_baseline": None, "dtype": "f32 (3xTF32 tcgen05)" if prec == 0 else "bf16",
             "data": "synthetic (seeded harness.hpp generator), random-init experts", "config": config,
             "e2e": e2e, "gpu_launches": args.steps, "gpu_launches_per_step": 1, "roofline": roof,
-            "clocks": clk.summary(), "setup_s": setup_s, "operator_event_ms_last_launch": st_ms,
+            "clocks": dict(clk.summary(), in_kernel=kclk), "setup_s": setup_s, "operator_event_ms_last_launch": st_ms,
             "operator": {k: info[k] for k in ("capacity", "packet_rows", "ctas_per_rank", "smem_bytes")},
             "schedules": {"overlapped_ms": ms, "sequential_ms": seq_ms, "sequential_over_overlapped": seq_ms / ms,
                           "sequential_nccl_ms": bulk_ms,

@@ -15,3 +15,6 @@ timeout 900 ncu --set full --import-source on --clock-control none -k regex:fdmo
     -o gpurun_out/prof_${TAG}_full_bf16 python tools/run_layer.py 16384 128 1 3 > gpurun_out/ncu_full_${TAG}_bf16.log 2>&1
 tail -c 600 gpurun_out/bench_${TAG}.json; echo; tail -c 300 gpurun_out/bench_${TAG}_bf16.json; echo
 tail -2 gpurun_out/ncu_full_${TAG}.log
+timeout 300 python tools/phase_trace.py 16384 128 0 > gpurun_out/phase_${TAG}_fp32.txt 2>&1
+timeout 300 python tools/phase_trace.py 16384 128 1 > gpurun_out/phase_${TAG}_bf16.txt 2>&1
+timeout 600 python tools/configs.py > gpurun_out/configs_${TAG}.jsonl 2>&1
