@@ -647,7 +647,7 @@ class Operator:
         t[:, :7] -= t0
         t[:, 20:27] -= t0
         t[:, 28:32] = np.where(t[:, 28:32] > 0, t[:, 28:32] - t0, 0)   # tensor-core gate logits done / staged
-        t[:, 36:38] = np.where(t[:, 36:38] > 0, t[:, 36:38] - t0, 0)   # distributed full-exact pass
+        t[:, 36:40] = np.where(t[:, 36:40] > 0, t[:, 36:40] - t0, 0)   # full-exact pass; gate roles start / epilogue done
         return t
 
     def events(self, local_rank: int = 0) -> np.ndarray:

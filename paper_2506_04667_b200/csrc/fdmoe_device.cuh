@@ -44,7 +44,8 @@ enum WaitSlot : int {
     kTrGateLoad = 29,                                             // tensor-core logits staged for routing
     kTrGateDecide = 30, kTrGateExp = 31,                          // thread-route decisions / exps done
     kTrClk0 = 32, kTrClkFfn0, kTrClkFfn1, kTrClkEnd,              // clock64 at start / FFN start / FFN end / end
-    kTrFullChains = 36, kTrFullRouted = 37                        // distributed full-exact pass: chains claimed / routed
+    kTrFullChains = 36, kTrFullRouted = 37,                       // distributed full-exact pass: chains claimed / routed
+    kTrGateStart = 38, kTrGateEpiDone = 39                        // tensor-core gate: roles start / epilogue done
 };
 
 enum Prec : int { kFP32 = 0, kBF16 = 1 };

@@ -2296,6 +2296,63 @@ __device__ void gemm_mma_fp32_pp(const LaunchParams& P, uint8_t* ring, GemmCtrl&
         }
         ++ntile;
         const int nk = (task_k(P, type) + Cfg::BK - 1) / Cfg::BK;
+        if (type == kGateTask) {
+            // Gate tile (M = 128 token rows in TMEM, N = gate_n experts from smem): the main products of every
+            // 64-K stage go to a FRESH accumulator (rotating acc; the gate epilogue folds each stage in RN FP32,
+            // mma_gate_tile's scheme), the corrections accumulate over the tile in kTmemCorr, fresh after the
+            // previous tile's fold (cempty). Token stages carry one ready/done per stage (both warps commit).
+            const uint32_t gdesc = umma_idesc(2u, kBF, (uint32_t)P.gate_n);
+            for (int kb = 0; kb < nk; ++kb) {
+                const long long g0 = clog ? pclk() : 0;
+                if (par == 0 && !FD_TIMED_WAIT(w_acc, wwait(&G.tempty[acc], accphase ^ 1u, P.abort_flag))) return;
+                const long long g1 = clog ? pclk() : 0;
+                if (!FD_TIMED_WAIT(w_x, wwait(&G.ready[stage], phase, P.abort_flag))) return;
+                const long long g2 = clog ? pclk() : 0;
+                if (!FD_TIMED_WAIT(w_x, wwait(&G.afull[par], aph, P.abort_flag))) return;
+                const long long g3 = clog ? pclk() : 0;
+                if (started && !FD_TIMED_WAIT(w_x, wwait(&G.pp[par], pph, P.abort_flag))) return;
+                if (clog && lane == 0 && nlog < kChunkLog / 8) {
+                    // chunk log (development build), gate, rows [384 + 64 par, +64): per stage {acc wait,
+                    // token-plane wait, A wait, hand-off wait + issue}
+                    unsigned long long* o = clog + 4 * (3 * kChunkLog / 4 + par * (kChunkLog / 8) + nlog++);
+                    o[0] = g1 - g0; o[1] = g2 - g1; o[2] = g3 - g2; o[3] = pclk() - g3;
+                }
+                if (started) pph ^= 1u;
+                started = true;
+                tc_fence_after();
+                const uint32_t d_main = tmem + (uint32_t)(acc * kNT);
+                const uint64_t bd = umma_desc_kmajor(smem_u32(ring + stage * Cfg::STAGE_BYTES), 128) +
+                                    (uint64_t)((par * Cfg::ATOM_BYTES) >> 4);
+                const uint32_t main_acc = par == 0 ? 0u : 1u;
+                if (kb == 0 && par == 0) {   // corrections start fresh once the previous tile's fold freed them
+                    if (elect_one()) issue_half_fp32<true, false>(d_main, d_corr, a_half, bd, gdesc, 0u, 0u);
+                    __syncwarp();
+                    uint32_t cph = G.pp_cph;
+                    if (!FD_TIMED_WAIT(w_x, wwait(&G.cempty, cph ^ 1u, P.abort_flag))) return;
+                    cph ^= 1u;
+                    tc_fence_after();
+                    if (elect_one()) {
+                        issue_half_fp32<false, true>(d_main, d_corr, a_half, bd, gdesc, 0u, 0u);
+                        G.pp_cph = cph;
+                    }
+                } else if (elect_one()) {
+                    issue_half_fp32<true, true>(d_main, d_corr, a_half, bd, gdesc, main_acc, 1u);
+                }
+                __syncwarp();
+                if (elect_one()) {
+                    mma_commit(&G.aempty[par]);
+                    mma_commit(&G.done[stage]);
+                    mma_commit(&G.tfull[acc]);   // this stage's main partial (and at the last stage the corrections)
+                }
+                __syncwarp();
+                tc_fence_before();
+                if (lane == 0) mbar_arrive(&G.pp[par ^ 1]);
+                if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
+                aph ^= 1u;
+                if (++acc == kAccStages) { acc = 0; accphase ^= 1u; }
+            }
+            continue;
+        }
         const long long t_tile = clog ? pclk() : 0;
         long long s_tok = 0, s_a = 0, s_pp = 0;
         if (par == 0 && !FD_TIMED_WAIT(w_acc, wwait(&G.tempty[acc], accphase ^ 1u, P.abort_flag))) return;
@@ -2786,14 +2843,18 @@ __device__ void gate_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
 
 __device__ __forceinline__ void init_ctrl_fp32(GemmCtrl& G, uint32_t tmem_base, uint32_t tempty_count) {
     using Cfg = GemmCfg<kFP32>;
-    for (int i = 0; i < Cfg::STAGES; ++i) { mbar_init(&G.ready[i], ReadyCount<kFP32>::N); mbar_init(&G.done[i], 1); }
+    // the tensor-core gate runs on the two FP32 issuer warps (gemm_mma_fp32_pp): each commits every token stage
+    // (both read it: one atom each) and every per-stage accumulator, and both take tasks from the ring
+    for (int i = 0; i < Cfg::STAGES; ++i) { mbar_init(&G.ready[i], ReadyCount<kFP32>::N); mbar_init(&G.done[i], 2); }
     for (int i = 0; i < Cfg::WSTAGES; ++i) { mbar_init(&G.wfull[i], 1); mbar_init(&G.wempty[i], 4); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&G.afull[i], 4); mbar_init(&G.aempty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&G.afull[i], 4); mbar_init(&G.aempty[i], 1); mbar_init(&G.pp[i], 1); }
     mbar_init(&G.cempty, 4);
-    for (int i = 0; i < kAccStages; ++i) { mbar_init(&G.tfull[i], 1); mbar_init(&G.tempty[i], tempty_count); }
-    for (int i = 0; i < kTaskRing; ++i) { mbar_init(&G.qfull[i], 1); mbar_init(&G.qempty[i], kTaskConsumers); }
+    for (int i = 0; i < kAccStages; ++i) { mbar_init(&G.tfull[i], 2); mbar_init(&G.tempty[i], tempty_count); }
+    for (int i = 0; i < kTaskRing; ++i) { mbar_init(&G.qfull[i], 1); mbar_init(&G.qempty[i], TaskConsumers<kFP32>::N); }
     for (int i = 0; i < kTaskRing; ++i) { mbar_init(&G.sfull[i], 1); mbar_init(&G.sempty[i], 1); }
     G.tmem_base = tmem_base;
+    G.pp_corr = 0;
+    G.pp_cph = 0;
 }
 
 // ================================================================ phase 4: combine
@@ -2951,14 +3012,16 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
         __syncthreads();
         int tokA, tokB, b0, b1;
         gate_token_range(P, cta, tokA, tokB, b0, b1);
-        if (warp == kWarpMma) {
-            gemm_mma<kFP32>(P, ring, GG, trace, nullptr);
+        if (tid == 0) trace[kTrGateStart] = globaltimer();
+        if (warp == kWarpMma || warp == kWarpTmem) {
+            gemm_mma_fp32_pp(P, ring, GG, trace, (cta == 0 && R.chunklog) ? R.chunklog : nullptr, warp == kWarpMma ? 0 : 1);
         } else if (warp == kWarpProducer) {
             if ((tid & 31) == 0) gate_producer(P, R, rl, ring, GG, tokA, tokB);
         } else if (warp >= kWarpConv0 && warp < kWarpConv0 + 4) {
             gemm_wconvert<kFP32>(P, ring, GG, nullptr, nullptr, R.gate_na);
         } else if (warp >= kWarpEpi0 && warp < kWarpEpi0 + 4) {
             gate_epilogue(P, R, GG);
+            if (tid == kWarpEpi0 * 32) trace[kTrGateEpiDone] = globaltimer();
         }
         tc_fence_before();
         __syncthreads();

@@ -6,7 +6,9 @@ import paper_2506_04667_b200 as fd
 fd.select_library(fd._build.DEV_LIB)   # per-role wait accounting is compiled into the development build only
 S, E = int(sys.argv[1]) if len(sys.argv) > 1 else 16384, int(sys.argv[2]) if len(sys.argv) > 2 else 128
 prec = int(sys.argv[3]) if len(sys.argv) > 3 else 0
-cfg = fd.MoeConfig(tokens_per_device=S, embed_dim=2048, ffn_dim=2048, experts_total=E, devices=1, topk=2,
+Hd = int(sys.argv[4]) if len(sys.argv) > 4 else 2048
+Dd = int(sys.argv[5]) if len(sys.argv) > 5 else 2048
+cfg = fd.MoeConfig(tokens_per_device=S, embed_dim=Hd, ffn_dim=Dd, experts_total=E, devices=1, topk=2,
                    tile_rows=128, tile_cols=64, precision=prec)
 op = fd.Operator(cfg); op.set_weights(fd.make_model(cfg))
 x = torch.from_numpy(fd.make_shards(cfg)[0]).cuda(); y = torch.empty_like(x)
@@ -19,7 +21,7 @@ names = ["start", "gate", "barrier", "dispatch", "ffn", "combine", "end"]
 print("kernel ms", op.last_kernel_ms())
 for i, n in enumerate(names):
     print(f"{n:9s} min {t[:, i].min():9.1f}  med {np.median(t[:, i]):9.1f}  max {t[:, i].max():9.1f} us")
-for i, n in ((28, "gate-tc-logits"), (29, "gate-load"), (30, "gate-decide"), (31, "gate-exp"), (24, "gate-route"), (25, "gate-pairs"), (26, "gate-full"), (36, "full-chains"), (37, "full-routed"), (20, "prefix"), (21, "slots"), (22, "slot-barrier"), (23, "push")):
+for i, n in ((38, "gate-roles0"), (39, "gate-epi-end"), (28, "gate-tc-logits"), (29, "gate-load"), (30, "gate-decide"), (31, "gate-exp"), (24, "gate-route"), (25, "gate-pairs"), (26, "gate-full"), (36, "full-chains"), (37, "full-routed"), (20, "prefix"), (21, "slots"), (22, "slot-barrier"), (23, "push")):
     print(f"{n:12s} min {t[:, i].min():9.1f}  med {np.median(t[:, i]):9.1f}  max {t[:, i].max():9.1f} us")
 g = t[:, 1]
 worst = int(np.argmax(g))
