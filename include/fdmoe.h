@@ -238,9 +238,8 @@ typedef struct fdmoe_info {
     int32_t smem_bytes;
     int32_t num_sms;
     int32_t ranks_per_launch;
-    int32_t fused_combine;  /* 1: overlapped launches fold the combine into the GEMM1 epilogues (FP32 mode,
-                             * k <= 2, every rank of the group on one device); sequential launches never do
-                             * (bf16 keeps the combine phase: its FFN is epilogue-bound) */
+    int32_t fused_combine;  /* 1: overlapped launches fold the combine into the GEMM1 epilogues (k <= 2, every
+                             * rank of the group on one device; both precisions); sequential launches never do */
 } fdmoe_info;
 fdmoe_status fdmoe_get_info(fdmoe_handle* h, fdmoe_info* info);
 /* Device time of the most recent forward's launch (CUDA events on the launching stream;

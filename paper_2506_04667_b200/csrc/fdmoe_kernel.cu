@@ -3088,12 +3088,10 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
         if ((tid & 31) == 0) gemm_signal(P, R, G, s_stat);
     } else if (warp >= kWarpEpi0 && warp < kWarpEpi0 + 4) {
         unsigned long long* elog = (cta == 0 && R.chunklog) ? R.chunklog : nullptr;
-        if constexpr (PREC == kFP32) {   // bf16 keeps the combine phase (measured: fusing does not pay)
-            if (P.fused_combine) gemm_epilogue<PREC, true>(P, R, G, s_stat, trace, elog);
-            else gemm_epilogue<PREC, false>(P, R, G, s_stat, trace, elog);
-        } else {
-            gemm_epilogue<PREC, false>(P, R, G, s_stat, trace, elog);
-        }
+        // both precisions fuse the combine into the GEMM1 epilogue when the launch holds every rank (round 2: bf16
+        // c4 0.672 -> 0.651 ms, c5 0.170 -> 0.158 ms, tools/ab.py; in round 1 its epilogue-bound FFN did not gain)
+        if (P.fused_combine) gemm_epilogue<PREC, true>(P, R, G, s_stat, trace, elog);
+        else gemm_epilogue<PREC, false>(P, R, G, s_stat, trace, elog);
     }
     __syncthreads();
     // sequential schedule: every rank's expert compute drains before any combine starts

@@ -626,8 +626,7 @@ static fdmoe_status launch_all(fdmoe_handle* h, const float* const* in_dev, floa
         p.sequential = sequential ? 1 : 0;
         p.trace_events = trace_events ? 1 : 0;
         p.straggler_rank = straggler_rank;
-        p.fused_combine = (d.prec == FDMOE_FP32 && d.k <= 2 && !sequential && (int64_t)g.members.size() == d.P &&
-                           h->n_local == d.P) ? 1 : 0;
+        p.fused_combine = (d.k <= 2 && !sequential && (int64_t)g.members.size() == d.P && h->n_local == d.P) ? 1 : 0;
         if (p.fused_combine) p.zero_target = (++g.zero_seq) * (uint32_t)g.ctas_per_rank;
         p.exact_gate = (opts && opts->exact_gate) ? 1 : 0;
         {   // certified-gate bound coefficients (fdmoe_kernel.cu, phase 1)
@@ -887,8 +886,8 @@ fdmoe_status fdmoe_get_info(fdmoe_handle* h, fdmoe_info* info) {
     info->smem_bytes = h->groups[0].smem;
     info->num_sms = h->groups[0].num_sms;
     info->ranks_per_launch = (int32_t)h->groups[0].members.size();
-    info->fused_combine = (h->dm.prec == FDMOE_FP32 && h->dm.k <= 2 &&
-                           (int64_t)h->groups[0].members.size() == h->dm.P && h->n_local == h->dm.P) ? 1 : 0;
+    info->fused_combine = (h->dm.k <= 2 && (int64_t)h->groups[0].members.size() == h->dm.P && h->n_local == h->dm.P)
+                              ? 1 : 0;
     return FDMOE_OK;
 }
 
