@@ -235,9 +235,19 @@ def main():
                        precision=prec)
     import torch
     import torch.distributed as dist
+    # FDMOE_BENCH_SHARED_GPU=1 (tests only): every rank on GPU 0 and gloo for the bootstrap, so the multi-process
+    # path of this script (CUDA-IPC heaps, cross-process peer stores) runs on a single-GPU box. NCCL refuses two
+    # ranks on one device; the contexts time-slice the GPU, so its timings mean nothing.
+    shared_gpu = world > 1 and os.environ.get("FDMOE_BENCH_SHARED_GPU") == "1"
+    if shared_gpu:
+        local = 0
+    red_dev = "cpu" if shared_gpu else "cuda"
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     def barrier():
         if world > 1:
@@ -304,7 +314,7 @@ def main():
     except Exception as ex:  # noqa: BLE001
         kclk = {"unavailable": str(ex)}
     if world > 1:
-        ms = fdist.max_over_ranks(ms, device="cuda")
+        ms = fdist.max_over_ranks(ms, device=red_dev)
     tokens_per_step = cfg.tokens_per_device * n
     value = tokens_per_step / (ms * 1e-3)
     # cross-check: the operator's own events around its launches (same stream)
@@ -328,7 +338,7 @@ def main():
     op.sync()
     seq_ms = ev0.elapsed_time(ev1) / seq_steps
     if world > 1:
-        seq_ms = fdist.max_over_ranks(seq_ms, device="cuda")
+        seq_ms = fdist.max_over_ranks(seq_ms, device=red_dev)
 
     # ---------------------------------------------------------------- bulk-synchronous NCCL baseline (§8 f1)
     # separate library kernels + NCCL all_to_all_single for dispatch and combine (bulksync.py): the
@@ -347,7 +357,7 @@ def main():
         torch.cuda.synchronize()
         bulk_ms = ev0.elapsed_time(ev1) / seq_steps
         if world > 1:
-            bulk_ms = fdist.max_over_ranks(bulk_ms, device="cuda")
+            bulk_ms = fdist.max_over_ranks(bulk_ms, device=red_dev)
         del bulk
         torch.cuda.empty_cache()
 
@@ -372,8 +382,8 @@ def main():
         _forward_host(fd, op, host_in, outs_h)
     sync_s = (time.perf_counter() - t0) / 3
     if world > 1:
-        e2e_s = fdist.max_over_ranks(e2e_s, device="cuda")
-        sync_s = fdist.max_over_ranks(sync_s, device="cuda")
+        e2e_s = fdist.max_over_ranks(e2e_s, device=red_dev)
+        sync_s = fdist.max_over_ranks(sync_s, device=red_dev)
     e2e = {"value": tokens_per_step / e2e_s, "unit": "tokens/s",
            "h2d_bytes_per_step": int(sum(x.nbytes for x in host_in)),
            "d2h_bytes_per_step": int(sum(x.nbytes for x in outs_h)), "ms_per_step": e2e_s * 1e3,

@@ -163,6 +163,7 @@ enum DebugBits : int {
     kDbgGateNoEpi = 2048,     // tensor-core gate: epilogue skips the per-stage TMEM fold (timing only)
     kDbgEvictNormal = 4096,   // token / C1 / gate-row loads with evict_normal instead of evict_last (A/B)
     kDbgInjectOversub = 8192, // fault injection: CTA 0 over-counts one kept row of expert 0 (ProtocolError test)
+    kDbgSimtGate = 16384,     // A/B: SIMT certified gate logits instead of the tensor-core gate
 };
 
 // Ablation bits are honoured only by the development library (libfdmoe_dev.so, -DFDMOE_DEV);

@@ -661,6 +661,7 @@ static fdmoe_status launch_all(fdmoe_handle* h, const float* const* in_dev, floa
 #ifdef FDMOE_DEV
         const char* dbg = getenv("FDMOE_DEBUG");   // ablation switches (tools/ablate.py): development library only
         p.debug = dbg ? atoi(dbg) : 0;
+        if (p.debug & kDbgSimtGate) p.gate_tc = 0;   // A/B: the SIMT certified gate instead of the tensor-core one
 #else
         p.debug = 0;
 #endif

@@ -213,3 +213,21 @@ def test_cpp_dropin_forward_on_gpu(tmp_path):
         for d in range(P):
             _check_outputs(got[d], rr["outputs"][d])
             assert np.array_equal(tab[d].reshape(-1), rr["table_token"][d].reshape(-1).astype(np.int32))
+
+
+def test_bench_torchrun_two_processes_one_gpu():
+    """bench.py's multi-process path (the driver's SCALE run: one rank per process, CUDA-IPC heaps, peer stores,
+    max-over-ranks timing) under torchrun with 2 ranks sharing GPU 0 (FDMOE_BENCH_SHARED_GPU: gloo bootstrap,
+    since NCCL refuses two ranks on one device). Checks the bench line, not the (time-sliced) numbers."""
+    port = _free_port()
+    env = dict(os.environ, FDMOE_BENCH_SHARED_GPU="1", PYTHONPATH=ROOT)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"), "--gpus", "2", "--tokens", "1024",
+           "--experts", "8", "--steps", "3", "--warmup", "3", "--e2e-steps", "2", "--no-bulksync", "--no-cpu-baseline"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["config"]["ep"] == 2
+    assert line["value"] > 0 and line["e2e"]["value"] > 0 and line["gpu_launches_per_step"] == 1

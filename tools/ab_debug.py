@@ -8,7 +8,9 @@ import paper_2506_04667_b200 as fd
 fd.select_library(fd._build.DEV_LIB)
 prec, S, E = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
 sets = [int(b) for b in sys.argv[4].split(",")]
-cfg = fd.MoeConfig(tokens_per_device=S, embed_dim=2048, ffn_dim=2048, experts_total=E, devices=1, topk=2,
+Hd = int(sys.argv[5]) if len(sys.argv) > 5 else 2048
+Dd = int(sys.argv[6]) if len(sys.argv) > 6 else 2048
+cfg = fd.MoeConfig(tokens_per_device=S, embed_dim=Hd, ffn_dim=Dd, experts_total=E, devices=1, topk=2,
                    tile_rows=128, tile_cols=64, precision=prec)
 op = fd.Operator(cfg); op.set_weights(fd.make_model(cfg))
 x = torch.from_numpy(fd.make_shards(cfg)[0]).cuda(); y = torch.empty_like(x)
