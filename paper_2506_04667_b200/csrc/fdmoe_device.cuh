@@ -164,6 +164,7 @@ enum DebugBits : int {
     kDbgEvictNormal = 4096,   // token / C1 / gate-row loads with evict_normal instead of evict_last (A/B)
     kDbgInjectOversub = 8192, // fault injection: CTA 0 over-counts one kept row of expert 0 (ProtocolError test)
     kDbgSimtGate = 16384,     // A/B: SIMT certified gate logits instead of the tensor-core gate
+    kDbgHalfCorr = 32768,     // timing only: the FP32 FFN issues half of its correction MMAs (results wrong)
 };
 
 // Ablation bits are honoured only by the development library (libfdmoe_dev.so, -DFDMOE_DEV);
@@ -386,6 +387,12 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
         ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
           "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
         : "memory");
+}
+// 32 lanes x 8 consecutive 32-bit columns from registers.
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+                 "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
 }
 // 32 lanes x 32 consecutive 32-bit columns from registers.
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {

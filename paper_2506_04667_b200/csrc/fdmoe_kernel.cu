@@ -89,6 +89,23 @@ __device__ __forceinline__ float activation(int act, float x) {
 __device__ __forceinline__ float tf32_hi(float x) {
     return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
+// Two floats as a bf16x2 word (round to nearest even): the low half holds the even-k element.
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+    __nv_bfloat162 p = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&p);
+}
+// FFN FP32-accurate operand format (round 2, "tf32 main + bf16 corrections"): x = x_hi + x_lo with x_hi = tf32(x)
+// (round to nearest) and x_lo exact. The main products w_hi*x_hi run as kind::tf32 MMAs (exact products); the two
+// correction products w_lo*x_hi + w_hi*x_lo, 2^-11 smaller, run as kind::f16 bf16 x bf16 MMAs on bf16(w_lo),
+// bf16(x_hi), bf16(w_hi), bf16(x_lo): one K=16 MMA does the work of two K=8 tf32 ones, so a 32-k half-stage is
+// 4 tf32 + 4 bf16 MMAs (512 tensor cycles) instead of 12 tf32 (768). Each bf16 product is within 2^-20 |w||x| of
+// the exact correction product (bf16 keeps 8 of the operand's bits), below the tf32 main accumulator's per-MMA
+// truncation (profiles/r02_numerics.md, tools/dev/numerics_model.py). Planes per 32-k atom (128 bytes per row):
+//   plane 0: x_hi as tf32 (FP32 words)
+//   plane 1: bf16(x_hi[k0..31]) (64 bytes) | bf16(x_lo[k0..31]) (64 bytes)
+// and the TMEM weight half-stage: cols [0,32) w_hi tf32, [32,48) bf16x2(w_lo), [48,64) bf16x2(w_hi).
+// The tensor-core gate keeps all-tf32 corrections (its certificate, k1_tc, is derived for them).
+constexpr bool kCorrBf16 = true;
 
 // ---------------------------------------------------------------- error / watchdog
 __device__ __noinline__ void raise_error(const LaunchParams& P, const RankCtx& R, uint32_t code, uint32_t where,
@@ -1443,15 +1460,23 @@ __device__ void push_phase(const LaunchParams& P, const RankCtx& R, const float*
             if (P.prec == kFP32) {
                 float4* dhi = reinterpret_cast<float4*>(hb + R.hl.x[par][0]) + row * H4;
                 float4* dlo = reinterpret_cast<float4*>(hb + R.hl.x[par][1]) + row * H4;
+                uint2* dlb = reinterpret_cast<uint2*>(hb + R.hl.x[par][1]) + row * (size_t)(H / 2);
 #pragma unroll
                 for (int u = 0; u < kPushUnroll; ++u) {
-                    if (c0 + 32 * u >= H4) break;
+                    const int c = c0 + 32 * u;
+                    if (c >= H4) break;
                     float4 h, l;
                     h.x = tf32_hi(v[u].x); h.y = tf32_hi(v[u].y); h.z = tf32_hi(v[u].z); h.w = tf32_hi(v[u].w);
                     l.x = __fsub_rn(v[u].x, h.x); l.y = __fsub_rn(v[u].y, h.y);
                     l.z = __fsub_rn(v[u].z, h.z); l.w = __fsub_rn(v[u].w, h.w);
-                    dhi[c0 + 32 * u] = h;
-                    dlo[c0 + 32 * u] = l;
+                    dhi[c] = h;
+                    if (kCorrBf16) {   // plane 1: [bf16 x_hi | bf16 x_lo] per 32-k group (16 uint2 per group)
+                        const size_t gb = (size_t)(c >> 3) * 16 + (c & 7);
+                        dlb[gb] = make_uint2(pack_bf16x2(h.x, h.y), pack_bf16x2(h.z, h.w));
+                        dlb[gb + 8] = make_uint2(pack_bf16x2(l.x, l.y), pack_bf16x2(l.z, l.w));
+                    } else {
+                        dlo[c] = l;
+                    }
                 }
             } else {
                 uint2* d = reinterpret_cast<uint2*>(hb + R.hl.x[par][0]) + row * H4;
@@ -1859,9 +1884,30 @@ __device__ void gemm_wconvert(const LaunchParams& P, uint8_t* ring, GemmCtrl& G,
                     if (!FD_TIMED_WAIT(w_a, mbar_wait(&G.aempty[ast], aphase ^ 1u, P.abort_flag))) return;
                     tc_fence_after();
                     const uint32_t col = tmem + lane_addr + Cfg::TMEM_A0 + ast * Cfg::A_COLS;
+                    if (kCorrBf16 && type != kGateTask && !FD_DBG(kDbgNoConvert)) {
+                        // FFN: w_hi tf32 in [0, 32), bf16x2(w_lo) in [32, 48), bf16x2(w_hi) in [48, 64)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            uint32_t hi[16], lp[8], hp[8];
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                const float4 v = c[at][h * 4 + i];
+                                const float h0 = tf32_hi(v.x), h1 = tf32_hi(v.y), h2 = tf32_hi(v.z), h3 = tf32_hi(v.w);
+                                hi[i * 4 + 0] = __float_as_uint(h0); hi[i * 4 + 1] = __float_as_uint(h1);
+                                hi[i * 4 + 2] = __float_as_uint(h2); hi[i * 4 + 3] = __float_as_uint(h3);
+                                lp[i * 2 + 0] = pack_bf16x2(__fsub_rn(v.x, h0), __fsub_rn(v.y, h1));
+                                lp[i * 2 + 1] = pack_bf16x2(__fsub_rn(v.z, h2), __fsub_rn(v.w, h3));
+                                hp[i * 2 + 0] = pack_bf16x2(h0, h1);
+                                hp[i * 2 + 1] = pack_bf16x2(h2, h3);
+                            }
+                            tmem_st16(col + h * 16, hi);
+                            tmem_st8(col + Cfg::ATOM_K + h * 8, lp);
+                            tmem_st8(col + Cfg::ATOM_K + 16 + h * 8, hp);
+                        }
+                    }
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {   // 16 K values per half atom
-                        if (FD_DBG(kDbgNoConvert)) break;
+                        if (FD_DBG(kDbgNoConvert) || (kCorrBf16 && type != kGateTask)) break;
                         uint32_t hi[16], lo[16];
 #pragma unroll
                         for (int i = 0; i < 4; ++i) {
@@ -2019,6 +2065,38 @@ __device__ __forceinline__ void issue_fp32_steady(uint32_t d_main, uint32_t d_co
     }
 }
 
+// bf16-correction half-stage (kCorrBf16, FFN tiles): MAIN = 4 tf32 MMAs w_hi*x_hi into d_main; CORR = 2 bf16 MMAs
+// bf16(w_lo)*bf16(x_hi) then 2 bf16(w_hi)*bf16(x_lo) (K = 16 each) into d_corr. bdesc: the atom's plane-0
+// descriptor (plane 1 is PLANE_BYTES further).
+template <bool MAIN, bool CORR>
+__device__ __forceinline__ void issue_half_b16(uint32_t d_main, uint32_t d_corr, uint32_t a_half, uint64_t bdesc,
+                                               uint32_t idesc, uint32_t main_acc, uint32_t corr_acc) {
+    using Cfg = GemmCfg<kFP32>;
+    constexpr uint32_t kIdescB = umma_idesc(1u, kBF, kNT);
+    if (CORR) {
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks)   // bf16(w_lo) * bf16(x_hi): A cols 32 + 8 ks, plane-1 bytes 32 ks
+            mma_bf16_ts(d_corr, a_half + Cfg::ATOM_K + ks * 8, bdesc + ((Cfg::PLANE_BYTES + ks * 32) >> 4), kIdescB,
+                        ks == 0 ? corr_acc : 1u);
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks)   // bf16(w_hi) * bf16(x_lo): A cols 48 + 8 ks, plane-1 bytes 64 + 32 ks
+            mma_bf16_ts(d_corr, a_half + Cfg::ATOM_K + 16 + ks * 8, bdesc + ((Cfg::PLANE_BYTES + 64 + ks * 32) >> 4),
+                        kIdescB, 1u);
+    }
+    if (MAIN) {
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)   // w_hi * x_hi (tf32)
+            mma_tf32_ts(d_main, a_half + ks * Cfg::KSTEP, bdesc + ((ks * 32) >> 4), idesc, ks == 0 ? main_acc : 1u);
+    }
+}
+// the FFN's half-stage in either format
+template <bool MAIN, bool CORR>
+__device__ __forceinline__ void issue_half_ffn(uint32_t d_main, uint32_t d_corr, uint32_t a_half, uint64_t bdesc,
+                                               uint32_t idesc, uint32_t main_acc, uint32_t corr_acc) {
+    if (kCorrBf16) issue_half_b16<MAIN, CORR>(d_main, d_corr, a_half, bdesc, idesc, main_acc, corr_acc);
+    else issue_half_fp32<MAIN, CORR>(d_main, d_corr, a_half, bdesc, idesc, main_acc, corr_acc);
+}
+
 constexpr int kCorrInMainMax = 2;
 struct MmaFp32State {
     int stage = 0, ah = 0;
@@ -2064,13 +2142,14 @@ __device__ __forceinline__ bool mma_tile_fp32(const LaunchParams& P, uint8_t* ri
             const bool stage_end = at == Cfg::NATOM - 1;
             if (corr_free) {
                 if (elect_one()) {
-                    issue_fp32_steady<0, 12>(d_main, d_corr, a_half, bd, idesc);
+                    if (kCorrBf16) issue_half_b16<true, true>(d_main, d_corr, a_half, bd, idesc, 1u, 1u);
+                    else issue_fp32_steady<0, 12>(d_main, d_corr, a_half, bd, idesc);
                     mma_commit(&G.aempty[st.ah]);
                     if (stage_end) mma_commit(&G.done[st.stage]);   // token + weight stage reusable
                 }
                 __syncwarp();
             } else {
-                if (elect_one()) issue_half_fp32<true, false>(d_main, d_corr, a_half, bd, idesc, first ? 0u : 1u, 0u);
+                if (elect_one()) issue_half_ffn<true, false>(d_main, d_corr, a_half, bd, idesc, first ? 0u : 1u, 0u);
                 __syncwarp();
                 const int h = kb * Cfg::NATOM + at;
                 corr_free = wtest(&G.cempty, st.cph ^ 1u);
@@ -2081,9 +2160,9 @@ __device__ __forceinline__ bool mma_tile_fp32(const LaunchParams& P, uint8_t* ri
                 if (corr_free) {
                     st.cph ^= 1u;
                     tc_fence_after();
-                    if (elect_one()) issue_half_fp32<false, true>(d_main, d_corr, a_half, bd, idesc, 0u, 0u);
+                    if (elect_one()) issue_half_ffn<false, true>(d_main, d_corr, a_half, bd, idesc, 0u, 0u);
                 } else {   // corrections of this half-stage ride in the main accumulator
-                    if (elect_one()) issue_half_fp32<false, true>(d_main, d_main, a_half, bd, idesc, 0u, 1u);
+                    if (elect_one()) issue_half_ffn<false, true>(d_main, d_main, a_half, bd, idesc, 0u, 1u);
                 }
                 __syncwarp();
                 wcommit(&G.aempty[st.ah]);
@@ -2375,14 +2454,15 @@ __device__ void gemm_mma_fp32_pp(const LaunchParams& P, uint8_t* ring, GemmCtrl&
             const bool last = kb + 1 == nk;
             if (kb > 0) {   // steady state: both accumulators accumulate
                 if (elect_one()) {
-                    issue_fp32_steady<0, 12>(d_main, d_corr, a_half, bd, idesc);
+                    if (kCorrBf16) issue_half_b16<true, true>(d_main, d_corr, a_half, bd, idesc, 1u, 1u);
+                    else issue_fp32_steady<0, 12>(d_main, d_corr, a_half, bd, idesc);
                     mma_commit(&G.aempty[par]);
                     mma_commit(&G.done[slot]);
                     if (last) mma_commit(&G.tfull[acc]);
                 }
                 __syncwarp();
             } else if (par == 0) {   // h = 0: main starts fresh; corrections fresh if the fold freed kTmemCorr
-                if (elect_one()) issue_half_fp32<true, false>(d_main, d_corr, a_half, bd, idesc, 0u, 0u);
+                if (elect_one()) issue_half_ffn<true, false>(d_main, d_corr, a_half, bd, idesc, 0u, 0u);
                 __syncwarp();
                 uint32_t cph = G.pp_cph;
                 const bool corr_free = wtest(&G.cempty, cph ^ 1u);
@@ -2391,8 +2471,8 @@ __device__ void gemm_mma_fp32_pp(const LaunchParams& P, uint8_t* ring, GemmCtrl&
                     tc_fence_after();
                 }
                 if (elect_one()) {
-                    if (corr_free) issue_half_fp32<false, true>(d_main, d_corr, a_half, bd, idesc, 0u, 0u);
-                    else issue_half_fp32<false, true>(d_main, d_main, a_half, bd, idesc, 0u, 1u);   // ride in main
+                    if (corr_free) issue_half_ffn<false, true>(d_main, d_corr, a_half, bd, idesc, 0u, 0u);
+                    else issue_half_ffn<false, true>(d_main, d_main, a_half, bd, idesc, 0u, 1u);   // ride in main
                     mma_commit(&G.aempty[par]);
                     mma_commit(&G.done[slot]);
                     if (last) mma_commit(&G.tfull[acc]);
@@ -2403,7 +2483,7 @@ __device__ void gemm_mma_fp32_pp(const LaunchParams& P, uint8_t* ring, GemmCtrl&
             } else {   // h = 1: corrections into kTmemCorr -- fresh if h = 0 could not, after the fold (blocking)
                 uint32_t cph = G.pp_cph;
                 const bool corr_free = G.pp_corr != 0;
-                if (elect_one()) issue_half_fp32<true, false>(d_main, d_corr, a_half, bd, idesc, 1u, 0u);
+                if (elect_one()) issue_half_ffn<true, false>(d_main, d_corr, a_half, bd, idesc, 1u, 0u);
                 __syncwarp();
                 if (!corr_free) {
                     if (!FD_TIMED_WAIT(w_x, wwait(&G.cempty, cph ^ 1u, P.abort_flag))) return;
@@ -2411,7 +2491,7 @@ __device__ void gemm_mma_fp32_pp(const LaunchParams& P, uint8_t* ring, GemmCtrl&
                     tc_fence_after();
                 }
                 if (elect_one()) {
-                    issue_half_fp32<false, true>(d_main, d_corr, a_half, bd, idesc, 0u, corr_free ? 1u : 0u);
+                    issue_half_ffn<false, true>(d_main, d_corr, a_half, bd, idesc, 0u, corr_free ? 1u : 0u);
                     mma_commit(&G.aempty[par]);
                     mma_commit(&G.done[slot]);
                     if (last) mma_commit(&G.tfull[acc]);
@@ -2505,6 +2585,9 @@ __device__ __forceinline__ void fold_corr(uint32_t t_main, uint32_t t_corr) {
 template <int PREC, int ACT>
 __device__ __forceinline__ void epi_gemm0(const uint32_t (&r)[32], uint32_t vmask, float bias, float* hi, float* lo,
                                           __nv_bfloat16* bf, int D) {
+    // C1 plane 1 in the bf16-correction format: this thread's feature is lane (feat % 32) of its 32-k group
+    const int lane = threadIdx.x & 31;
+    __nv_bfloat16* lb = reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<uint8_t*>(lo) - 4 * lane) + lane;
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
         if (!(vmask & (1u << i))) continue;
@@ -2513,7 +2596,12 @@ __device__ __forceinline__ void epi_gemm0(const uint32_t (&r)[32], uint32_t vmas
         if (PREC == kFP32) {
             const float h = tf32_hi(v);
             hi[o] = h;
-            lo[o] = __fsub_rn(v, h);
+            if (kCorrBf16) {
+                lb[2 * o] = __float2bfloat16_rn(h);                  // bf16 x_hi at byte 2 * lane of the group
+                lb[2 * o + 32] = __float2bfloat16_rn(__fsub_rn(v, h));   // bf16 x_lo at byte 64 + 2 * lane
+            } else {
+                lo[o] = __fsub_rn(v, h);
+            }
         } else {
             bf[o] = __float2bfloat16_rn(v);
         }

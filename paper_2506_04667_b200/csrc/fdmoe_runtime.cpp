@@ -979,7 +979,12 @@ fdmoe_status fdmoe_debug_gemm(int32_t prec, int32_t K, const float* W, const flo
             std::memcpy(&h, &u, 4);
             const float l = X[i] - h;
             std::memcpy(&xh[i * 4], &h, 4);
-            std::memcpy(&xl[i * 4], &l, 4);
+            // plane 1 in the FFN's bf16-correction format (fdmoe_kernel.cu kCorrBf16): per row and 32-k group,
+            // bf16(x_hi[k]) at byte 2 (k % 32), bf16(x_lo[k]) at byte 64 + 2 (k % 32)
+            const size_t row = i / (size_t)K, k = i % (size_t)K, g = row * (size_t)K * 4 + (k / 32) * 128;
+            const uint16_t bh = to_bf16(h), bl = to_bf16(l);
+            std::memcpy(&xl[g + 2 * (k % 32)], &bh, 2);
+            std::memcpy(&xl[g + 64 + 2 * (k % 32)], &bl, 2);
         } else {
             const uint16_t bw = to_bf16(W[i]), bx = to_bf16(X[i]);
             std::memcpy(&wp[i * 2], &bw, 2);

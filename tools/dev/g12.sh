@@ -1,0 +1,6 @@
+set -u
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_baseline.py -q --timeout 400 2>&1 | tail -15
+cat gpurun_out/numerics.jsonl 2>/dev/null | tail -12
+timeout 600 python bench.py --no-cpu-baseline --no-bulksync --e2e-steps 2 > gpurun_out/g12_bench.json 2> gpurun_out/g12_bench.err; echo bench rc $?
+python -c "import json; d=json.load(open('gpurun_out/g12_bench.json')); print(d['ms_per_step'], d['roofline']['frac'], d['clocks']['in_kernel'])"
+timeout 300 python tools/phase_trace.py 16384 128 0 2>&1 | grep "effective\|^ffn \|^dispatch\|kernel"
