@@ -1881,29 +1881,33 @@ __device__ void gemm_wconvert(const LaunchParams& P, uint8_t* ring, GemmCtrl& G,
                 // each released to the MMA warp on its own so the ring runs half a stage ahead
 #pragma unroll
                 for (int at = 0; at < Cfg::NATOM; ++at) {
+                    // FFN (kCorrBf16): the atom's A operand is formed in registers BEFORE the slot wait, so only
+                    // the two TMEM stores sit between the MMAs freeing the slot and the slot refilled (the
+                    // converter's aempty -> afull turnaround must fit one 8-MMA half-stage of the other issuer)
+                    const bool ffn_b16 = kCorrBf16 && type != kGateTask && !FD_DBG(kDbgNoConvert);
+                    uint32_t fhi[32], fcb[32];   // w_hi tf32 | bf16x2(w_lo) (16 words), bf16x2(w_hi) (16 words)
+                    if (ffn_b16) {
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const float4 v = c[at][i];
+                            const float h0 = tf32_hi(v.x), h1 = tf32_hi(v.y), h2 = tf32_hi(v.z), h3 = tf32_hi(v.w);
+                            fhi[i * 4 + 0] = __float_as_uint(h0); fhi[i * 4 + 1] = __float_as_uint(h1);
+                            fhi[i * 4 + 2] = __float_as_uint(h2); fhi[i * 4 + 3] = __float_as_uint(h3);
+                            fcb[i * 2 + 0] = pack_bf16x2(__fsub_rn(v.x, h0), __fsub_rn(v.y, h1));
+                            fcb[i * 2 + 1] = pack_bf16x2(__fsub_rn(v.z, h2), __fsub_rn(v.w, h3));
+                            fcb[16 + i * 2 + 0] = pack_bf16x2(h0, h1);
+                            fcb[16 + i * 2 + 1] = pack_bf16x2(h2, h3);
+                        }
+                    }
+                    const long long a0 = pclk();
                     if (!FD_TIMED_WAIT(w_a, mbar_wait(&G.aempty[ast], aphase ^ 1u, P.abort_flag))) return;
+                    const long long a1 = pclk();
                     tc_fence_after();
                     const uint32_t col = tmem + lane_addr + Cfg::TMEM_A0 + ast * Cfg::A_COLS;
-                    if (kCorrBf16 && type != kGateTask && !FD_DBG(kDbgNoConvert)) {
+                    if (ffn_b16) {
                         // FFN: w_hi tf32 in [0, 32), bf16x2(w_lo) in [32, 48), bf16x2(w_hi) in [48, 64)
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            uint32_t hi[16], lp[8], hp[8];
-#pragma unroll
-                            for (int i = 0; i < 4; ++i) {
-                                const float4 v = c[at][h * 4 + i];
-                                const float h0 = tf32_hi(v.x), h1 = tf32_hi(v.y), h2 = tf32_hi(v.z), h3 = tf32_hi(v.w);
-                                hi[i * 4 + 0] = __float_as_uint(h0); hi[i * 4 + 1] = __float_as_uint(h1);
-                                hi[i * 4 + 2] = __float_as_uint(h2); hi[i * 4 + 3] = __float_as_uint(h3);
-                                lp[i * 2 + 0] = pack_bf16x2(__fsub_rn(v.x, h0), __fsub_rn(v.y, h1));
-                                lp[i * 2 + 1] = pack_bf16x2(__fsub_rn(v.z, h2), __fsub_rn(v.w, h3));
-                                hp[i * 2 + 0] = pack_bf16x2(h0, h1);
-                                hp[i * 2 + 1] = pack_bf16x2(h2, h3);
-                            }
-                            tmem_st16(col + h * 16, hi);
-                            tmem_st8(col + Cfg::ATOM_K + h * 8, lp);
-                            tmem_st8(col + Cfg::ATOM_K + 16 + h * 8, hp);
-                        }
+                        tmem_st32(col, fhi);
+                        tmem_st32(col + Cfg::ATOM_K, fcb);
                     }
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {   // 16 K values per half atom
@@ -1927,6 +1931,12 @@ __device__ void gemm_wconvert(const LaunchParams& P, uint8_t* ring, GemmCtrl& G,
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&G.afull[ast]);
+                    if (clog && threadIdx.x == kWarpConv0 * 32 && type != kGateTask && nlog < 64) {
+                        // chunk log (development build), rows [320, 384): per FFN half-stage {weight-stage wait,
+                        // A-slot wait, convert + store + arrive, clock at the A wait}
+                        unsigned long long* o = clog + 4 * (320 + nlog++);
+                        o[0] = at == 0 ? c1 - c0 : 0; o[1] = a1 - a0; o[2] = pclk() - a1; o[3] = a0;
+                    }
                     if (++ast == Cfg::A_SLOTS) { ast = 0; aphase ^= 1u; }
                 }
                 continue;
@@ -3171,7 +3181,7 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
     } else if (warp == kWarpProducer) {
         if ((tid & 31) == 0) gemm_producer<PREC>(P, R, ring, G, trace);
     } else if (warp >= kWarpConv0 && warp < kWarpConv0 + 4) {
-        gemm_wconvert<PREC>(P, ring, G, trace, nullptr);
+        gemm_wconvert<PREC>(P, ring, G, trace, (cta == 0 && R.chunklog) ? R.chunklog : nullptr);
     } else if (warp == kWarpSignal) {
         if ((tid & 31) == 0) gemm_signal(P, R, G, s_stat);
     } else if (warp >= kWarpEpi0 && warp < kWarpEpi0 + 4) {
