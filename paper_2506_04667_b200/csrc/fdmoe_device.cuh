@@ -116,6 +116,7 @@ struct alignas(64) RankCtx {
     uint32_t* full_ctr;        // [3] distributed full-exact pass: tokens listed, chains claimed, chains done
     int32_t* full_list;        // [kFullCap] tokens needing every expert's exact logit (ties / near-ties)
     float* full_z;             // [kFullCap][E_total] their exact logits (reference chain, gate.hpp:77-81)
+    float* epart;              // [ctas][128 cols][128 rows] FP32 FFN: the first-half main partial of the CTA's tile
     uint32_t ev_cap;
     int32_t rank;
 };

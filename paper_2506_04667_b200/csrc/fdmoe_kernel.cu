@@ -106,6 +106,12 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
 // and the TMEM weight half-stage: cols [0,32) w_hi tf32, [32,48) bf16x2(w_lo), [48,64) bf16x2(w_hi).
 // The tensor-core gate keeps all-tf32 corrections (its certificate, k1_tc, is derived for them).
 constexpr bool kCorrBf16 = true;
+// FFN FP32 main accumulation split over K into the two TMEM main buffers (gemm_mma_fp32_pp / gemm_epilogue)
+#ifdef FDMOE_NO_SPLITK
+constexpr bool kSplitK = false;
+#else
+constexpr bool kSplitK = true;
+#endif
 
 // ---------------------------------------------------------------- error / watchdog
 __device__ __noinline__ void raise_error(const LaunchParams& P, const RankCtx& R, uint32_t code, uint32_t where,
@@ -833,6 +839,78 @@ __device__ void route_softmax(const LaunchParams& P, const RankCtx& R, const Gat
     }
 }
 
+// FP32 mode: the reference logits of the k picks of every thread-certified token of a sub-tile, one thread per
+// (token, pick) running the reference chain z = sum over x ascending of fl(a_x w_x) (gate.hpp:77-81) over token /
+// Wg^T row chunks staged in smem (3-deep cp.async ring, 32 x per chunk), and the tokens' combine weights
+// recomputed from them: w_j = e_j / (e_0 + e_1) with e_j = expf(z_j - z_0) (the softmax sum cancels). The
+// certified z~ is ~1e-6 off the reference chain, and the weights derived from it carried that error into rare
+// cancellation-dominated output elements above the FP32 bound (tools/dev/parity_wide.py: worst 1.07 of the bound
+// with z~ weights, 0.54 with exact ones). Routing is unaffected (it is certified bit-exact either way).
+__device__ void gate_pick_weights(const LaunchParams& P, const RankCtx& R, const float* __restrict__ A,
+                                  const GateSmem& g, int tok0, int ts, const int* sDec) {
+    const int H = P.H, E = P.E, K = P.k, tid = threadIdx.x;
+    constexpr int XC = 32, PITCH = 36, NST = 3;
+    float* ring = g.sA;
+    const int rows = ts + E;
+    const int stage_f = rows * PITCH;
+    int* plist = reinterpret_cast<int*>(ring + NST * stage_f);   // [2 ts]: (t << 16) | expert, -1 = none
+    float* zp = reinterpret_cast<float*>(plist + 2 * kGateSubMax);
+    for (int i = tid; i < 2 * ts; i += kThreads) {
+        const int t = i >> 1, j = i & 1;
+        const int d = sDec[t];
+        plist[i] = (d < 0 || j >= K) ? -1 : ((t << 16) | (j == 0 ? (d & 0xffff) : (d >> 16)));
+    }
+    __syncthreads();   // sDec lives in the staging area the ring overwrites
+    const int my = tid < 2 * ts ? plist[tid] : -1;
+    const int mt = my >> 16, me = my & 0xffff;
+    auto load = [&](int st, int c) {
+        float* b = ring + st * stage_f;
+        const int x0 = c * XC;
+        for (int i = tid; i < rows * (XC / 4); i += kThreads) {
+            const int r = i >> 3, q = i & 7;
+            const float* src = r < ts ? A + (size_t)(tok0 + r) * H + x0 + 4 * q : R.wgT + (size_t)(r - ts) * H + x0 + 4 * q;
+            cp_async16(b + r * PITCH + 4 * q, src, true);
+        }
+        cp_async_commit();
+    };
+    const int nch = H / XC;   // H % 32 == 0 (envelope)
+    float z = 0.0f;
+    load(0, 0);
+    if (nch > 1) load(1, 1); else cp_async_commit();
+    for (int c = 0; c < nch; ++c) {
+        if (c + 2 < nch) load((c + 2) % NST, c + 2); else cp_async_commit();
+        cp_async_wait<2>();
+        __syncthreads();
+        if (my >= 0) {
+            const float* ar = ring + (c % NST) * stage_f + mt * PITCH;
+            const float* wr = ring + (c % NST) * stage_f + (ts + me) * PITCH;
+#pragma unroll
+            for (int q = 0; q < XC / 4; ++q) {
+                const float4 a4 = *reinterpret_cast<const float4*>(ar + 4 * q);
+                const float4 w4 = *reinterpret_cast<const float4*>(wr + 4 * q);
+                z = __fadd_rn(z, __fmul_rn(a4.x, w4.x));
+                z = __fadd_rn(z, __fmul_rn(a4.y, w4.y));
+                z = __fadd_rn(z, __fmul_rn(a4.z, w4.z));
+                z = __fadd_rn(z, __fmul_rn(a4.w, w4.w));
+            }
+        }
+        __syncthreads();
+    }
+    cp_async_wait<0>();
+    if (my >= 0) zp[tid] = z;
+    __syncthreads();
+    if (K == 2)
+        for (int t = tid; t < ts; t += kThreads) {
+            if (plist[2 * t] < 0) continue;
+            const size_t tok = (size_t)tok0 + t;
+            const float e1 = expf_glibc(__fsub_rn(zp[2 * t + 1], zp[2 * t]), g.tab);   // e_0 = expf(0) = 1
+            const float den = __fadd_rn(1.0f, e1);
+            R.pick_w[tok * 2] = __fdiv_rn(1.0f, den);
+            R.pick_w[tok * 2 + 1] = __fdiv_rn(e1, den);
+        }
+    __syncthreads();
+}
+
 // Exact reference logits of np (token, expert) pairs: thread p runs pair p's separately-rounded
 // chain over x ascending (gate.hpp:77-81), rows staged through smem in x-chunks (A row and Wg^T row).
 __device__ void gate_pairs_exact(const LaunchParams& P, const RankCtx& R, const float* __restrict__ A,
@@ -1204,6 +1282,9 @@ __device__ void gate_phase(const LaunchParams& P, const RankCtx& R, const float*
             __syncthreads();
             if (tid == 0) R.trace[(size_t)cta * kTracePts + kTrGateDecide] = globaltimer();
             route_softmax(P, R, g, Lp, tokA + s0, ts, sDec, sZ0, cta);
+#ifndef FDMOE_NO_PICKW
+            if (P.prec == kFP32) gate_pick_weights(P, R, A, g, tokA + s0, ts, sDec);
+#endif
         } else {
             for (int t = warp; t < ts; t += kWarps) {
                 const int r = route_certified(P, R, g.sL + t * Ep, tokA + s0 + t, t, g, &s_np);
@@ -2362,6 +2443,7 @@ __device__ void gemm_mma_fp32_pp(const LaunchParams& P, uint8_t* ring, GemmCtrl&
     uint32_t qphase = 0;
     int acc = 0;
     uint32_t accphase = 0;
+    uint32_t tph0 = 0, tph1 = 0;   // FFN split-K buffers' tempty phases
     int stage = 0;
     uint32_t phase = 0, aph = 0, pph = 0;
     bool started = par == 1;   // par 0's very first half-stage has no predecessor
@@ -2444,10 +2526,20 @@ __device__ void gemm_mma_fp32_pp(const LaunchParams& P, uint8_t* ring, GemmCtrl&
         }
         const long long t_tile = clog ? pclk() : 0;
         long long s_tok = 0, s_a = 0, s_pp = 0;
-        if (par == 0 && !FD_TIMED_WAIT(w_acc, wwait(&G.tempty[acc], accphase ^ 1u, P.abort_flag))) return;
         const long long t_acc = clog ? pclk() : 0;
-        const uint32_t d_main = tmem + (uint32_t)(acc * kNT);
+        // Split-K main accumulation (FFN): the first nk0 = nk/2 stages' main products go to buffer 0, the rest to
+        // buffer 1; the epilogue saves buffer 0's partial mid-tile and adds it in RN at the end. Each buffer then
+        // sees half the truncating MMAs on a half-length partial sum (profiles/r02_numerics.md §5).
+        const int nk0 = kSplitK ? nk / 2 : 0;
         for (int kb = 0; kb < nk; ++kb) {
+            const int buf = kb < nk0 ? 0 : 1;
+            if (par == 0 && (kb == 0 || kb == nk0)) {   // buffer free (the epilogue read the previous tile's)
+                if (!FD_TIMED_WAIT(w_acc, wwait(&G.tempty[buf], (buf ? tph1 : tph0) ^ 1u, P.abort_flag))) return;
+            }
+            if (kb == 0 && nk0 > 0) tph0 ^= 1u;
+            if (kb == nk0) tph1 ^= 1u;
+            const uint32_t d_main = tmem + (uint32_t)(buf * kNT);
+            const bool buf_first = kb == nk0 && kb > 0;   // first stage into buffer 1 (par 0's MMAs start it fresh)
             const long long c0 = clog ? pclk() : 0;
             const int slot = stage * Cfg::NATOM + par;   // this warp's token atom of the stage (own ready/done)
             if (!FD_TIMED_WAIT(w_x, wwait(&G.ready[slot], phase, P.abort_flag))) return;
@@ -2462,13 +2554,17 @@ __device__ void gemm_mma_fp32_pp(const LaunchParams& P, uint8_t* ring, GemmCtrl&
             const uint64_t bd = umma_desc_kmajor(smem_u32(ring + stage * Cfg::STAGE_BYTES), 128) +
                                 (uint64_t)((par * Cfg::ATOM_BYTES) >> 4);
             const bool last = kb + 1 == nk;
+            const bool half_end = kb + 1 == nk0;   // buffer 0 complete after this stage
             if (kb > 0) {   // steady state: both accumulators accumulate
                 if (elect_one()) {
-                    if (kCorrBf16) issue_half_b16<true, true>(d_main, d_corr, a_half, bd, idesc, 1u, 1u);
-                    else issue_fp32_steady<0, 12>(d_main, d_corr, a_half, bd, idesc);
+                    const uint32_t macc = (buf_first && par == 0) ? 0u : 1u;
+                    if (kCorrBf16) issue_half_b16<true, true>(d_main, d_corr, a_half, bd, idesc, macc, 1u);
+                    else if (macc) issue_fp32_steady<0, 12>(d_main, d_corr, a_half, bd, idesc);
+                    else issue_half_fp32<true, true>(d_main, d_corr, a_half, bd, idesc, 0u, 1u);
                     mma_commit(&G.aempty[par]);
                     mma_commit(&G.done[slot]);
-                    if (last) mma_commit(&G.tfull[acc]);
+                    if (half_end) mma_commit(&G.tfull[0]);
+                    if (last) mma_commit(&G.tfull[1]);
                 }
                 __syncwarp();
             } else if (par == 0) {   // h = 0: main starts fresh; corrections fresh if the fold freed kTmemCorr
@@ -2485,7 +2581,8 @@ __device__ void gemm_mma_fp32_pp(const LaunchParams& P, uint8_t* ring, GemmCtrl&
                     else issue_half_ffn<false, true>(d_main, d_main, a_half, bd, idesc, 0u, 1u);   // ride in main
                     mma_commit(&G.aempty[par]);
                     mma_commit(&G.done[slot]);
-                    if (last) mma_commit(&G.tfull[acc]);
+                    if (half_end) mma_commit(&G.tfull[0]);
+                    if (last) mma_commit(&G.tfull[1]);
                     G.pp_corr = corr_free ? 1u : 0u;
                     G.pp_cph = cph;
                 }
@@ -2504,7 +2601,8 @@ __device__ void gemm_mma_fp32_pp(const LaunchParams& P, uint8_t* ring, GemmCtrl&
                     issue_half_ffn<false, true>(d_main, d_corr, a_half, bd, idesc, 0u, corr_free ? 1u : 0u);
                     mma_commit(&G.aempty[par]);
                     mma_commit(&G.done[slot]);
-                    if (last) mma_commit(&G.tfull[acc]);
+                    if (half_end) mma_commit(&G.tfull[0]);
+                    if (last) mma_commit(&G.tfull[1]);
                     G.pp_cph = cph;
                 }
                 __syncwarp();
@@ -2523,7 +2621,6 @@ __device__ void gemm_mma_fp32_pp(const LaunchParams& P, uint8_t* ring, GemmCtrl&
             o[0] = (unsigned long long)type | ((unsigned long long)(pclk() - t_tile) << 8);
             o[1] = t_acc - t_tile; o[2] = s_tok; o[3] = (unsigned long long)s_a | ((unsigned long long)s_pp << 32);
         }
-        if (++acc == kAccStages) { acc = 0; accphase ^= 1u; }
     }
 }
 
@@ -2575,6 +2672,31 @@ __device__ void gemm_signal(const LaunchParams& P, const RankCtx& R, GemmCtrl& G
 
 // FP32: add the tile's correction accumulator into its main accumulator in round-to-nearest FP32
 // (this warp's 32 TMEM lanes, 128 token columns), leaving the correction columns free.
+// buffer 1 (second-half main partial) += first-half partial (RN, from the CTA scratch) += corrections (RN)
+__device__ __forceinline__ void fold_corr_part(uint32_t t_main, uint32_t t_corr, const float* part) {
+#pragma unroll 1
+    for (int ch = 0; ch < kNT / 32; ++ch) {
+        uint32_t m[32], c[32];
+        tmem_ld32(t_main + ch * 32, m);
+        tmem_ld32(t_corr + ch * 32, c);
+        float pv[32];
+        if (part) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) pv[i] = part[(size_t)(ch * 32 + i) * kBF];
+        }
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            float v = __uint_as_float(m[i]);
+            if (part) v = __fadd_rn(pv[i], v);
+            m[i] = __float_as_uint(__fadd_rn(v, __uint_as_float(c[i])));
+        }
+        tmem_st32(t_main + ch * 32, m);
+    }
+    tmem_wait_st();
+    tc_fence_before();
+}
+
 __device__ __forceinline__ void fold_corr(uint32_t t_main, uint32_t t_corr) {
 #pragma unroll 1
     for (int ch = 0; ch < kNT / 32; ++ch) {
@@ -2630,6 +2752,7 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
     uint32_t qphase = 0;
     int acc = 0;
     uint32_t accphase = 0;
+    uint32_t tph0 = 0, tph1 = 0;   // FP32: the split-K buffers' tfull phases
     const uint32_t tmem = G.tmem_base;
     const int e_glob_base = R.rank * P.El;
     int sq = 0;
@@ -2665,13 +2788,39 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
             }
             return;
         }
-        if (!FD_TIMED_WAIT(w_acc, mbar_wait(&G.tfull[acc], accphase, P.abort_flag))) return;
-        tc_fence_after();
-        if constexpr (PREC == kFP32) {   // main += corrections (RN), then the MMA warp may reuse kTmemCorr
+        if constexpr (PREC == kFP32) {
+            // split-K main accumulators (gemm_mma_fp32_pp): buffer 0 holds the first nk/2 stages' main partial
+            // and completes mid-tile -- save it (this thread's feature row, [col][row] in the CTA's scratch) and
+            // free the buffer for the next tile; at the end buffer 1 += partial (RN), += corrections (RN)
+            acc = 1;
             const uint32_t lanes = (uint32_t)(wq * 32) << 16;
-            fold_corr(tmem + lanes + (uint32_t)(acc * kNT), tmem + lanes + kTmemCorr);
+            const int nk0 = kSplitK ? ((task_k(P, type) + GemmCfg<kFP32>::BK - 1) / GemmCfg<kFP32>::BK) / 2 : 0;
+            float* part = R.epart + (size_t)(blockIdx.x % P.ctas_per_rank) * kNT * kBF + et;
+            if (nk0 > 0) {
+                if (!FD_TIMED_WAIT(w_acc, mbar_wait(&G.tfull[0], tph0, P.abort_flag))) return;
+                tph0 ^= 1u;
+                tc_fence_after();
+#pragma unroll 1
+                for (int ch = 0; ch < kNT / 32; ++ch) {
+                    uint32_t m[32];
+                    tmem_ld32(tmem + lanes + (uint32_t)(ch * 32), m);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) part[(size_t)(ch * 32 + i) * kBF] = __uint_as_float(m[i]);
+                }
+                tc_fence_before();
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (et == 0) mbar_arrive(&G.tempty[0]);
+            }
+            if (!FD_TIMED_WAIT(w_acc, mbar_wait(&G.tfull[1], tph1, P.abort_flag))) return;
+            tph1 ^= 1u;
+            tc_fence_after();
+            fold_corr_part(tmem + lanes + (uint32_t)kNT, tmem + lanes + kTmemCorr, nk0 > 0 ? part : nullptr);
             __syncwarp();
             if ((et & 31) == 0) mbar_arrive(&G.cempty);
+        } else {
+            if (!FD_TIMED_WAIT(w_acc, mbar_wait(&G.tfull[acc], accphase, P.abort_flag))) return;
+            tc_fence_after();
         }
         if (FUSED && type == 1 && !zero_seen) {
             for (int r = 0; r < P.nranks; ++r)
@@ -2795,7 +2944,7 @@ __device__ void gemm_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
             o[0] = type; o[1] = e_loop - tb0; o[2] = e_ld; o[3] = pclk() - e_bar;
         }
         if (++q == kTaskRing) { q = 0; qphase ^= 1u; }
-        if (++acc == kAccStages) { acc = 0; accphase ^= 1u; }
+        if (PREC != kFP32 && ++acc == kAccStages) { acc = 0; accphase ^= 1u; }
     }
 }
 

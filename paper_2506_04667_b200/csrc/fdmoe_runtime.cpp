@@ -125,6 +125,7 @@ struct RankRes {
     DevEvent* ev = nullptr;
     int32_t* full_list = nullptr;
     float* full_z = nullptr;
+    float* epart = nullptr;
     uint32_t ev_cap = 0;
     int ctas = 0;
     uint8_t* ctrl = nullptr;        // bar | heads | err | stats | sent | g0done
@@ -240,6 +241,7 @@ fdmoe_status alloc_rank(fdmoe_handle* h, RankRes& r, int ctas_per_rank) {
     parts.push_back({(void**)&r.blk_ready, (size_t)(d.S + kGateTok - 1) / kGateTok * 4});
     parts.push_back({(void**)&r.full_list, (size_t)kFullCap * 4});
     parts.push_back({(void**)&r.full_z, (size_t)kFullCap * d.E * 4});
+    parts.push_back({(void**)&r.epart, (size_t)ctas_per_rank * kNT * kBF * 4});
     parts.push_back({(void**)&r.ctrl, ctrl_bytes(d)});
     parts.push_back({(void**)&r.in_buf, (size_t)d.S * d.H * 4});
     parts.push_back({(void**)&r.out_buf, (size_t)d.S * d.H * 4});
@@ -307,6 +309,7 @@ fdmoe_status build_ctx(fdmoe_handle* h) {
             c.full_ctr = reinterpret_cast<uint32_t*>(r.ctrl + ctrl_ev_ctr(d) + 8);   // [3], inside the 64 spare bytes
             c.full_list = r.full_list;
             c.full_z = r.full_z;
+            c.epart = r.epart;
             c.bar = reinterpret_cast<unsigned long long*>(r.ctrl + kCtrlBar);
             c.gemm_head = reinterpret_cast<uint32_t*>(r.ctrl + kCtrlGemm);
             c.comb_head = reinterpret_cast<uint32_t*>(r.ctrl + kCtrlComb);

@@ -116,3 +116,24 @@ def test_baseline_config(name):
         st.update({"rank": d, "rows": "all" if full else int(got.shape[0]), "forward_s": t_gpu})
         record(name, st)
         check_outputs(prec, st)
+
+
+@pytest.mark.parametrize("name,seed,nrows", [("c2", 1, 4096), ("c3_p4", 0, 3072), ("c4_p1", 1, 6144)])
+def test_wide_rows(name, seed, nrows):
+    """Beyond the sampled rows: thousands of contiguous token rows (the kept-pick region) at the configurations and
+    seeds whose worst elements came closest to the FP32 bound before the split-K main accumulation and the exact
+    pick weights (tools/dev/parity_wide.py, profiles/r02_numerics.md §5): every element within the bound."""
+    S, H, D, E, P, prec, _ = CONFIGS[name]
+    cfg = fd.MoeConfig(tokens_per_device=S, embed_dim=H, ffn_dim=D, experts_total=E, devices=P, topk=2,
+                       capacity_factor=1.0, precision=prec, seed=seed)
+    model = fd.make_model(cfg)
+    shards = fd.make_shards(cfg)
+    res = fd.forward(cfg, shards, model)
+    for d in range(P):
+        want_route = check_routing(cfg, shards[d], model, res.gates[d])
+        rows = np.arange(min(nrows, S))
+        want = po.ffn_rows(shards[d], model, cfg, want_route, rows, threads=THREADS)
+        st = error_stats(res.outputs[d][rows], want, prec)
+        st.update({"rank": d, "rows": int(rows.size), "seed": seed})
+        record(name + "_wide", st)
+        check_outputs(prec, st)
