@@ -846,8 +846,10 @@ __device__ void route_softmax(const LaunchParams& P, const RankCtx& R, const Gat
 // certified z~ is ~1e-6 off the reference chain, and the weights derived from it carried that error into rare
 // cancellation-dominated output elements above the FP32 bound (tools/dev/parity_wide.py: worst 1.07 of the bound
 // with z~ weights, 0.54 with exact ones). Routing is unaffected (it is certified bit-exact either way).
+// It also runs the sub-tile's candidate (token, expert) pairs of the undecided tokens (g.sPT / g.sPE, np of them,
+// results to g.sPZ) -- the pair pass -- as a second chain per thread over the same staged rows.
 __device__ void gate_pick_weights(const LaunchParams& P, const RankCtx& R, const float* __restrict__ A,
-                                  const GateSmem& g, int tok0, int ts, const int* sDec) {
+                                  const GateSmem& g, int tok0, int ts, const int* sDec, int np) {
     const int H = P.H, E = P.E, K = P.k, tid = threadIdx.x;
     constexpr int XC = 32, PITCH = 36, NST = 3;
     float* ring = g.sA;
@@ -863,6 +865,7 @@ __device__ void gate_pick_weights(const LaunchParams& P, const RankCtx& R, const
     __syncthreads();   // sDec lives in the staging area the ring overwrites
     const int my = tid < 2 * ts ? plist[tid] : -1;
     const int mt = my >> 16, me = my & 0xffff;
+    const int cp_t = tid < np ? g.sPT[tid] - tok0 : -1, cp_e = tid < np ? g.sPE[tid] : 0;   // candidate pair
     auto load = [&](int st, int c) {
         float* b = ring + st * stage_f;
         const int x0 = c * XC;
@@ -874,16 +877,17 @@ __device__ void gate_pick_weights(const LaunchParams& P, const RankCtx& R, const
         cp_async_commit();
     };
     const int nch = H / XC;   // H % 32 == 0 (envelope)
-    float z = 0.0f;
+    float z = 0.0f, z2 = 0.0f;
     load(0, 0);
     if (nch > 1) load(1, 1); else cp_async_commit();
     for (int c = 0; c < nch; ++c) {
         if (c + 2 < nch) load((c + 2) % NST, c + 2); else cp_async_commit();
         cp_async_wait<2>();
         __syncthreads();
+        const float* st = ring + (c % NST) * stage_f;
         if (my >= 0) {
-            const float* ar = ring + (c % NST) * stage_f + mt * PITCH;
-            const float* wr = ring + (c % NST) * stage_f + (ts + me) * PITCH;
+            const float* ar = st + mt * PITCH;
+            const float* wr = st + (ts + me) * PITCH;
 #pragma unroll
             for (int q = 0; q < XC / 4; ++q) {
                 const float4 a4 = *reinterpret_cast<const float4*>(ar + 4 * q);
@@ -894,10 +898,24 @@ __device__ void gate_pick_weights(const LaunchParams& P, const RankCtx& R, const
                 z = __fadd_rn(z, __fmul_rn(a4.w, w4.w));
             }
         }
+        if (cp_t >= 0) {
+            const float* ar = st + cp_t * PITCH;
+            const float* wr = st + (ts + cp_e) * PITCH;
+#pragma unroll
+            for (int q = 0; q < XC / 4; ++q) {
+                const float4 a4 = *reinterpret_cast<const float4*>(ar + 4 * q);
+                const float4 w4 = *reinterpret_cast<const float4*>(wr + 4 * q);
+                z2 = __fadd_rn(z2, __fmul_rn(a4.x, w4.x));
+                z2 = __fadd_rn(z2, __fmul_rn(a4.y, w4.y));
+                z2 = __fadd_rn(z2, __fmul_rn(a4.z, w4.z));
+                z2 = __fadd_rn(z2, __fmul_rn(a4.w, w4.w));
+            }
+        }
         __syncthreads();
     }
     cp_async_wait<0>();
     if (my >= 0) zp[tid] = z;
+    if (cp_t >= 0) g.sPZ[tid] = z2;
     __syncthreads();
     if (K == 2)
         for (int t = tid; t < ts; t += kThreads) {
@@ -1228,6 +1246,7 @@ __device__ void gate_phase(const LaunchParams& P, const RankCtx& R, const float*
             n_full += ts;
             continue;
         }
+        bool pairs_done = false;
         for (int t = tid; t < ts; t += kThreads) { g.sSab[t] = 0.0f; g.sTNC[t] = 0; }
         if (tid == 0) { s_np = 0; s_nfull = 0; }
         __syncthreads();
@@ -1283,7 +1302,11 @@ __device__ void gate_phase(const LaunchParams& P, const RankCtx& R, const float*
             if (tid == 0) R.trace[(size_t)cta * kTracePts + kTrGateDecide] = globaltimer();
             route_softmax(P, R, g, Lp, tokA + s0, ts, sDec, sZ0, cta);
 #ifndef FDMOE_NO_PICKW
-            if (P.prec == kFP32) gate_pick_weights(P, R, A, g, tokA + s0, ts, sDec);
+            if (P.prec == kFP32) {
+                const int npc = FD_DBG(kDbgGateNoFlush) ? 0 : min(s_np, kGatePairCap);
+                gate_pick_weights(P, R, A, g, tokA + s0, ts, sDec, npc <= kThreads ? npc : 0);
+                pairs_done = npc <= kThreads;
+            }
 #endif
         } else {
             for (int t = warp; t < ts; t += kWarps) {
@@ -1295,7 +1318,7 @@ __device__ void gate_phase(const LaunchParams& P, const RankCtx& R, const float*
         if (tid == 0) R.trace[(size_t)cta * kTracePts + kTrGateLogits] = globaltimer();
         const int np = min(s_np, kGatePairCap);
         if (np > 0 && !(FD_DBG(kDbgGateNoFlush))) {
-            gate_pairs_exact(P, R, A, g, np);
+            if (!pairs_done) gate_pairs_exact(P, R, A, g, np);   // (the FP32 pick pass ran them already)
             for (int t = warp; t < ts; t += kWarps) {
                 if (g.sTNC[t] == 0) continue;
                 ++n_pair_tok;
