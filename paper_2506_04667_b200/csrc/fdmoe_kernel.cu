@@ -851,7 +851,7 @@ __device__ void route_softmax(const LaunchParams& P, const RankCtx& R, const Gat
 __device__ void gate_pick_weights(const LaunchParams& P, const RankCtx& R, const float* __restrict__ A,
                                   const GateSmem& g, int tok0, int ts, const int* sDec, int np) {
     const int H = P.H, E = P.E, K = P.k, tid = threadIdx.x;
-    constexpr int XC = 32, PITCH = 36, NST = 3;
+    constexpr int XC = 32, PITCH = 36, NST = 3;   // (16-x chunks x 6 stages measured slower: per-chunk cost)
     float* ring = g.sA;
     const int rows = ts + E;
     const int stage_f = rows * PITCH;
@@ -870,7 +870,7 @@ __device__ void gate_pick_weights(const LaunchParams& P, const RankCtx& R, const
         float* b = ring + st * stage_f;
         const int x0 = c * XC;
         for (int i = tid; i < rows * (XC / 4); i += kThreads) {
-            const int r = i >> 3, q = i & 7;
+            const int r = i / (XC / 4), q = i % (XC / 4);
             const float* src = r < ts ? A + (size_t)(tok0 + r) * H + x0 + 4 * q : R.wgT + (size_t)(r - ts) * H + x0 + 4 * q;
             cp_async16(b + r * PITCH + 4 * q, src, true);
         }
@@ -878,11 +878,12 @@ __device__ void gate_pick_weights(const LaunchParams& P, const RankCtx& R, const
     };
     const int nch = H / XC;   // H % 32 == 0 (envelope)
     float z = 0.0f, z2 = 0.0f;
-    load(0, 0);
-    if (nch > 1) load(1, 1); else cp_async_commit();
+    for (int c = 0; c < NST - 1; ++c) {
+        if (c < nch) load(c, c); else cp_async_commit();
+    }
     for (int c = 0; c < nch; ++c) {
-        if (c + 2 < nch) load((c + 2) % NST, c + 2); else cp_async_commit();
-        cp_async_wait<2>();
+        if (c + NST - 1 < nch) load((c + NST - 1) % NST, c + NST - 1); else cp_async_commit();
+        cp_async_wait<NST - 1>();
         __syncthreads();
         const float* st = ring + (c % NST) * stage_f;
         if (my >= 0) {
