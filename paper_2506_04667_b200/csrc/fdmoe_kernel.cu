@@ -2458,6 +2458,20 @@ __device__ void gemm_mma(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, unsi
 // 12 MMAs run, and the hand-off (arrive -> wait, ~tens of cycles) is the only gap (tools/dev/pipe_rate3.py: 91.7 ->
 // 64.0 cycles per MMA for the full barrier protocol). Issue order is identical to one issuer's (results are
 // bit-identical); each warp commits its own MMAs.
+// Issuer hand-off on hardware named barriers (ids 2, 3; 64 threads = the two issuer warps): warp par waits on
+// barrier 2 + par, the other warp arrives on it after issuing its half-stage. A bar.sync completes in tens of
+// cycles (an mbarrier wake-up costs ~100-200), and the tensor queue holds only ~1-2 MMAs of the other warp's
+// half-stage (tools/dev/pipe_rate3.py: the named-barrier ping-pong issues at the tensor core's rate). A warp
+// leaving on abort arrives once more so that its partner is never left in bar.sync.
+__device__ __forceinline__ void pp_wait(int par) {
+    asm volatile("bar.sync %0, 64;" ::"r"(2 + par) : "memory");
+    tc_fence_after();
+}
+__device__ __forceinline__ void pp_signal(int par) {
+    tc_fence_before();
+    asm volatile("bar.arrive %0, 64;" ::"r"(2 + (par ^ 1)) : "memory");
+}
+
 __device__ void gemm_mma_fp32_pp(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, unsigned long long* trace,
                                  unsigned long long* clog, const int par) {
     using Cfg = GemmCfg<kFP32>;
@@ -2477,7 +2491,7 @@ __device__ void gemm_mma_fp32_pp(const LaunchParams& P, uint8_t* ring, GemmCtrl&
     const uint32_t a_half = tmem + Cfg::TMEM_A0 + (uint32_t)par * Cfg::A_COLS;
     const uint32_t idesc = Cfg::IDESC;
     while (true) {
-        if (!FD_TIMED_WAIT(w_task, wwait(&G.qfull[q], qphase, P.abort_flag))) return;
+        if (!FD_TIMED_WAIT(w_task, wwait(&G.qfull[q], qphase, P.abort_flag))) { pp_signal(par); return; }
         const int type = G.ring[q].type;
         __syncwarp();
         if (lane == 0) mbar_arrive(&G.qempty[q]);
@@ -2487,6 +2501,7 @@ __device__ void gemm_mma_fp32_pp(const LaunchParams& P, uint8_t* ring, GemmCtrl&
                 trace[kWaitMmaX] = w_x; trace[kWaitMmaA] = 0; trace[kWaitMmaAcc] = w_acc;
                 trace[kWaitMmaTask] = w_task; trace[kMmaTiles] = ntile;
             }
+            if (par == 0 && ntile > 0) pp_wait(0);   // every tile ends on warp 1: consume its last hand-off
             return;
         }
         ++ntile;
@@ -2499,20 +2514,19 @@ __device__ void gemm_mma_fp32_pp(const LaunchParams& P, uint8_t* ring, GemmCtrl&
             const uint32_t gdesc = umma_idesc(2u, kBF, (uint32_t)P.gate_n);
             for (int kb = 0; kb < nk; ++kb) {
                 const long long g0 = clog ? pclk() : 0;
-                if (par == 0 && !FD_TIMED_WAIT(w_acc, wwait(&G.tempty[acc], accphase ^ 1u, P.abort_flag))) return;
+                if (par == 0 && !FD_TIMED_WAIT(w_acc, wwait(&G.tempty[acc], accphase ^ 1u, P.abort_flag))) { pp_signal(par); return; }
                 const long long g1 = clog ? pclk() : 0;
-                if (!FD_TIMED_WAIT(w_x, wwait(&G.ready[stage], phase, P.abort_flag))) return;
+                if (!FD_TIMED_WAIT(w_x, wwait(&G.ready[stage], phase, P.abort_flag))) { pp_signal(par); return; }
                 const long long g2 = clog ? pclk() : 0;
-                if (!FD_TIMED_WAIT(w_x, wwait(&G.afull[par], aph, P.abort_flag))) return;
+                if (!FD_TIMED_WAIT(w_x, wwait(&G.afull[par], aph, P.abort_flag))) { pp_signal(par); return; }
                 const long long g3 = clog ? pclk() : 0;
-                if (started && !FD_TIMED_WAIT(w_x, wwait(&G.pp[par], pph, P.abort_flag))) return;
+                if (started) pp_wait(par);
                 if (clog && lane == 0 && nlog < kChunkLog / 8) {
                     // chunk log (development build), gate, rows [384 + 64 par, +64): per stage {acc wait,
                     // token-plane wait, A wait, hand-off wait + issue}
                     unsigned long long* o = clog + 4 * (3 * kChunkLog / 4 + par * (kChunkLog / 8) + nlog++);
                     o[0] = g1 - g0; o[1] = g2 - g1; o[2] = g3 - g2; o[3] = pclk() - g3;
                 }
-                if (started) pph ^= 1u;
                 started = true;
                 tc_fence_after();
                 const uint32_t d_main = tmem + (uint32_t)(acc * kNT);
@@ -2523,7 +2537,7 @@ __device__ void gemm_mma_fp32_pp(const LaunchParams& P, uint8_t* ring, GemmCtrl&
                     if (elect_one()) issue_half_fp32<true, false>(d_main, d_corr, a_half, bd, gdesc, 0u, 0u);
                     __syncwarp();
                     uint32_t cph = G.pp_cph;
-                    if (!FD_TIMED_WAIT(w_x, wwait(&G.cempty, cph ^ 1u, P.abort_flag))) return;
+                    if (!FD_TIMED_WAIT(w_x, wwait(&G.cempty, cph ^ 1u, P.abort_flag))) { pp_signal(par); return; }
                     cph ^= 1u;
                     tc_fence_after();
                     if (elect_one()) {
@@ -2541,7 +2555,7 @@ __device__ void gemm_mma_fp32_pp(const LaunchParams& P, uint8_t* ring, GemmCtrl&
                 }
                 __syncwarp();
                 tc_fence_before();
-                if (lane == 0) mbar_arrive(&G.pp[par ^ 1]);
+                pp_signal(par);
                 if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
                 aph ^= 1u;
                 if (++acc == kAccStages) { acc = 0; accphase ^= 1u; }
@@ -2558,7 +2572,7 @@ __device__ void gemm_mma_fp32_pp(const LaunchParams& P, uint8_t* ring, GemmCtrl&
         for (int kb = 0; kb < nk; ++kb) {
             const int buf = kb < nk0 ? 0 : 1;
             if (par == 0 && (kb == 0 || kb == nk0)) {   // buffer free (the epilogue read the previous tile's)
-                if (!FD_TIMED_WAIT(w_acc, wwait(&G.tempty[buf], (buf ? tph1 : tph0) ^ 1u, P.abort_flag))) return;
+                if (!FD_TIMED_WAIT(w_acc, wwait(&G.tempty[buf], (buf ? tph1 : tph0) ^ 1u, P.abort_flag))) { pp_signal(par); return; }
             }
             if (kb == 0 && nk0 > 0) tph0 ^= 1u;
             if (kb == nk0) tph1 ^= 1u;
@@ -2566,13 +2580,12 @@ __device__ void gemm_mma_fp32_pp(const LaunchParams& P, uint8_t* ring, GemmCtrl&
             const bool buf_first = kb == nk0 && kb > 0;   // first stage into buffer 1 (par 0's MMAs start it fresh)
             const long long c0 = clog ? pclk() : 0;
             const int slot = stage * Cfg::NATOM + par;   // this warp's token atom of the stage (own ready/done)
-            if (!FD_TIMED_WAIT(w_x, wwait(&G.ready[slot], phase, P.abort_flag))) return;
+            if (!FD_TIMED_WAIT(w_x, wwait(&G.ready[slot], phase, P.abort_flag))) { pp_signal(par); return; }
             const long long c1 = clog ? pclk() : 0;
-            if (!FD_TIMED_WAIT(w_x, wwait(&G.afull[par], aph, P.abort_flag))) return;
+            if (!FD_TIMED_WAIT(w_x, wwait(&G.afull[par], aph, P.abort_flag))) { pp_signal(par); return; }
             const long long c2 = clog ? pclk() : 0;
-            if (started && !FD_TIMED_WAIT(w_x, wwait(&G.pp[par], pph, P.abort_flag))) return;   // h-1 issued
+            if (started) pp_wait(par);   // h-1 issued
             const long long c3 = clog ? pclk() : 0;
-            if (started) pph ^= 1u;
             started = true;
             tc_fence_after();
             const uint64_t bd = umma_desc_kmajor(smem_u32(ring + stage * Cfg::STAGE_BYTES), 128) +
@@ -2617,7 +2630,7 @@ __device__ void gemm_mma_fp32_pp(const LaunchParams& P, uint8_t* ring, GemmCtrl&
                 if (elect_one()) issue_half_ffn<true, false>(d_main, d_corr, a_half, bd, idesc, 1u, 0u);
                 __syncwarp();
                 if (!corr_free) {
-                    if (!FD_TIMED_WAIT(w_x, wwait(&G.cempty, cph ^ 1u, P.abort_flag))) return;
+                    if (!FD_TIMED_WAIT(w_x, wwait(&G.cempty, cph ^ 1u, P.abort_flag))) { pp_signal(par); return; }
                     cph ^= 1u;
                     tc_fence_after();
                 }
@@ -2633,7 +2646,7 @@ __device__ void gemm_mma_fp32_pp(const LaunchParams& P, uint8_t* ring, GemmCtrl&
             }
             // hand-off: this half-stage is issued (tcgen05 ops ordered before the other warp's by the fence pair)
             tc_fence_before();
-            if (lane == 0) mbar_arrive(&G.pp[par ^ 1]);
+            pp_signal(par);
             s_tok += c1 - c0; s_a += c2 - c1; s_pp += c3 - c2;
             if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1u; }
             aph ^= 1u;
