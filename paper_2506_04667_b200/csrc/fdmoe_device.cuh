@@ -166,6 +166,7 @@ enum DebugBits : int {
     kDbgInjectOversub = 8192, // fault injection: CTA 0 over-counts one kept row of expert 0 (ProtocolError test)
     kDbgSimtGate = 16384,     // A/B: SIMT certified gate logits instead of the tensor-core gate
     kDbgHalfCorr = 32768,     // timing only: the FP32 FFN issues half of its correction MMAs (results wrong)
+    kDbgGateOnly = 65536,     // timing only: the launch ends after the tensor-core gate (gate role stamps in 20..23)
 };
 
 // Ablation bits are honoured only by the development library (libfdmoe_dev.so, -DFDMOE_DEV);

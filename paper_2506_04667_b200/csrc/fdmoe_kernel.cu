@@ -1918,6 +1918,15 @@ __device__ void gemm_producer(const LaunchParams& P, const RankCtx& R, uint8_t* 
 // so a warp's 128-bit loads are bank-conflict free.
 // Gate tiles (kGateTask, FP32 config) stream token rows through the same converter path; the
 // converters also accumulate each token row's sum of squares into gate_na (certified-gate bound).
+// Gate tiles also form their A words (x_hi tf32 | x_lo) in registers before the slot wait and store them with two
+// st32, like the FFN. Measured (tools/ab.py, product library, three boxes): FP32 c4 1.498 -> 1.468 ms, c2 0.412 ->
+// 0.400 ms, bf16 c4 0.650 -> 0.646 ms. The development build's gate timing (tools/dev/gate_only.py) did not move and
+// the product build's phase trace puts the gain in the FFN phase (~1.20 -> ~1.18 ms): the gate and the FFN share
+// this converter function, so it is a code-generation effect on the shared loop. -DFDMOE_GATE_PRECONV=0: the old path.
+#ifndef FDMOE_GATE_PRECONV
+#define FDMOE_GATE_PRECONV 1
+#endif
+constexpr bool kGatePreConv = FDMOE_GATE_PRECONV != 0;
 template <int PREC>
 __device__ void gemm_wconvert(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, unsigned long long* trace,
                               unsigned long long* clog, double* gate_na = nullptr) {
@@ -1990,7 +1999,22 @@ __device__ void gemm_wconvert(const LaunchParams& P, uint8_t* ring, GemmCtrl& G,
                     // the two TMEM stores sit between the MMAs freeing the slot and the slot refilled (the
                     // converter's aempty -> afull turnaround must fit one 8-MMA half-stage of the other issuer)
                     const bool ffn_b16 = kCorrBf16 && type != kGateTask && !FD_DBG(kDbgNoConvert);
+                    // gate tiles: the token atom's tf32 hi / lo words, also formed before the slot wait
+                    const bool gate_pre = kGatePreConv && type == kGateTask && !FD_DBG(kDbgNoConvert);
                     uint32_t fhi[32], fcb[32];   // w_hi tf32 | bf16x2(w_lo) (16 words), bf16x2(w_hi) (16 words)
+                    if (gate_pre) {
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const float4 v = c[at][i];
+                            const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const float hv = tf32_hi(vv[u]);
+                                fhi[i * 4 + u] = __float_as_uint(hv);
+                                fcb[i * 4 + u] = __float_as_uint(__fsub_rn(vv[u], hv));
+                            }
+                        }
+                    }
                     if (ffn_b16) {
 #pragma unroll
                         for (int i = 0; i < 8; ++i) {
@@ -2009,14 +2033,15 @@ __device__ void gemm_wconvert(const LaunchParams& P, uint8_t* ring, GemmCtrl& G,
                     const long long a1 = pclk();
                     tc_fence_after();
                     const uint32_t col = tmem + lane_addr + Cfg::TMEM_A0 + ast * Cfg::A_COLS;
-                    if (ffn_b16) {
+                    if (ffn_b16 || gate_pre) {
                         // FFN: w_hi tf32 in [0, 32), bf16x2(w_lo) in [32, 48), bf16x2(w_hi) in [48, 64)
+                        // gate: x_hi tf32 in [0, 32), x_lo FP32 in [32, 64)
                         tmem_st32(col, fhi);
                         tmem_st32(col + Cfg::ATOM_K, fcb);
                     }
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {   // 16 K values per half atom
-                        if (FD_DBG(kDbgNoConvert) || (kCorrBf16 && type != kGateTask)) break;
+                        if (FD_DBG(kDbgNoConvert) || (kCorrBf16 && type != kGateTask) || gate_pre) break;
                         uint32_t hi[16], lo[16];
 #pragma unroll
                         for (int i = 0; i < 4; ++i) {
@@ -2560,6 +2585,7 @@ __device__ void gemm_mma_fp32_pp(const LaunchParams& P, uint8_t* ring, GemmCtrl&
                 aph ^= 1u;
                 if (++acc == kAccStages) { acc = 0; accphase ^= 1u; }
             }
+            if (FD_DBG(kDbgGateOnly) && lane == 0) trace[20 + par] = globaltimer();   // tools/dev/gate_only.py
             continue;
         }
         const long long t_tile = clog ? pclk() : 0;
@@ -3097,6 +3123,7 @@ __device__ void gate_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
             if (++acc == kAccStages) { acc = 0; accphase ^= 1u; }
         }
         // the last stage's tfull also covered every correction MMA of the tile
+        if (FD_DBG(kDbgGateOnly) && et == 0) R.trace[(size_t)blockIdx.x % P.ctas_per_rank * kTracePts + 22] = globaltimer();
 #pragma unroll
         for (int ch = 0; ch < kBF / 16; ++ch) {
             if (ch * 16 < P.gate_n) {
@@ -3120,6 +3147,7 @@ __device__ void gate_epilogue(const LaunchParams& P, const RankCtx& R, GemmCtrl&
             else atomicMax(sp, __float_as_int(sab));   // non-negative floats order like their bits
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (FD_DBG(kDbgGateOnly) && et == 0) R.trace[(size_t)blockIdx.x % P.ctas_per_rank * kTracePts + 23] = globaltimer();
         if (et == 0) mbar_arrive(&G.qempty[q]);
         if (++q == kTaskRing) { q = 0; qphase ^= 1u; }
     }
@@ -3311,6 +3339,7 @@ __global__ void __launch_bounds__(kThreads, 1) fdmoe_layer_kernel(const __grid_c
         __syncthreads();
         tc_fence_after();
         if (tid == 0) trace[kTrGateTc] = globaltimer();
+        if (FD_DBG(kDbgGateOnly)) goto done;
     }
     // phase 1b: routing (certified from the tensor-core logits, or the SIMT gate), smem region as scratch
     gate_phase(P, R, A, cta, smem, s_stat, s_exp_tab);

@@ -22,3 +22,9 @@ for par in (0, 1):
     r = lg[384 + 64 * par:384 + 64 * par + 34].astype(np.int64)
     print(f"issuer {par}: per stage (cycles) acc wait / token-plane wait / A wait / hand-off wait + issue")
     print("  mean", r[2:32].mean(axis=0).round(0), " first rows:", r[:6].tolist())
+for par in (0, 1):
+    r = lg[384 + 64 * par:384 + 64 * (par + 1)].astype(np.int64)
+    nz = int((r.sum(axis=1) > 0).sum())
+    print(f"issuer {par}: {nz} logged stages, {r.sum() / 1e3:.1f} kcycles in the logged iterations")
+tr = op.trace(0).astype(np.float64)
+print(f"CTA 0 gate roles: start {tr[0, 38] / 1e3:.1f} us, epilogue done {tr[0, 39] / 1e3:.1f} us")

@@ -1,9 +1,11 @@
 """Phase breakdown of one layer launch from the device trace (per-CTA %globaltimer stamps)."""
-import sys, json, numpy as np
+import os, sys, json, numpy as np
 sys.path.insert(0, '.')
 import torch
 import paper_2506_04667_b200 as fd
-fd.select_library(fd._build.DEV_LIB)   # per-role wait accounting is compiled into the development build only
+# per-role wait accounting is compiled into the development build only; FDMOE_PHASE_LIB=<lib.so> traces another
+# build (phase stamps only: the wait columns read 0)
+fd.select_library(os.environ.get("FDMOE_PHASE_LIB", fd._build.DEV_LIB))
 S, E = int(sys.argv[1]) if len(sys.argv) > 1 else 16384, int(sys.argv[2]) if len(sys.argv) > 2 else 128
 prec = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 Hd = int(sys.argv[4]) if len(sys.argv) > 4 else 2048
@@ -36,3 +38,9 @@ for a, b, ca, cb, n in ((0, 3, 32, 33, "start..FFN"), (3, 4, 33, 34, "FFN"), (0,
 ffn_cyc = (t[:, 4] - t[:, 3]).mean() * 1e3 * 1.965   # ns -> cycles at max clock (approx)
 for i, n in enumerate(["mma<-tokens", "mma<-weights", "mma<-acc", "conv<-wTMA", "conv<-tmemA", "prod<-wslot", "prod<-xslot", "epi<-acc"]):
     print(f"wait {n:14s} mean {tr[:, 8 + i].mean() / 1e3:9.1f} kcyc  ({100 * tr[:, 8 + i].mean() / ffn_cyc:5.1f}% of FFN phase)")
+# distributed full-exact pass: the CTAs that finish it last (owner routing / late chains)
+nfull = np.round(tr[:, 27]).astype(int)
+print("full-exact tokens listed per CTA (nonzero):", {int(c): int(n) for c, n in enumerate(nfull) if n})
+for c in np.argsort(-t[:, 37])[:4]:
+    print(f"CTA {c:3d}: gate {t[c, 1]:.1f} full-chains {t[c, 36]:.1f} full-routed {t[c, 37]:.1f} "
+          f"prefix {t[c, 20]:.1f} us")
