@@ -1927,6 +1927,9 @@ __device__ void gemm_producer(const LaunchParams& P, const RankCtx& R, uint8_t* 
 #define FDMOE_GATE_PRECONV 1
 #endif
 constexpr bool kGatePreConv = FDMOE_GATE_PRECONV != 0;
+#ifndef FDMOE_GATE_NORM4
+#define FDMOE_GATE_NORM4 1
+#endif
 template <int PREC>
 __device__ void gemm_wconvert(const LaunchParams& P, uint8_t* ring, GemmCtrl& G, unsigned long long* trace,
                               unsigned long long* clog, double* gate_na = nullptr) {
@@ -1978,6 +1981,20 @@ __device__ void gemm_wconvert(const LaunchParams& P, uint8_t* ring, GemmCtrl& G,
 
             const long long c2 = pclk();
             if (PREC == kFP32 && g_norm && !FD_DBG(kDbgGateNoNorm)) {
+#if FDMOE_GATE_NORM4
+                // four independent 16-FMA chains (the 64-deep chain sat in front of the stage's TMEM stores);
+                // |a|^2 only feeds the certificate's rounded-up |a| (sqrt(na (1 + 1e-5))), any order is within it
+                float n0 = 0.0f, n1 = 0.0f, n2 = 0.0f, n3 = 0.0f;
+#pragma unroll
+                for (int at = 0; at < Cfg::NATOM; ++at)
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const float4 v = c[at][i];
+                        n0 = __fmaf_rn(v.x, v.x, n0); n1 = __fmaf_rn(v.y, v.y, n1);
+                        n2 = __fmaf_rn(v.z, v.z, n2); n3 = __fmaf_rn(v.w, v.w, n3);
+                    }
+                const float cs = (n0 + n1) + (n2 + n3);
+#else
                 float cs = 0.0f;
 #pragma unroll
                 for (int at = 0; at < Cfg::NATOM; ++at)
@@ -1987,6 +2004,7 @@ __device__ void gemm_wconvert(const LaunchParams& P, uint8_t* ring, GemmCtrl& G,
                         cs = __fmaf_rn(v.x, v.x, cs); cs = __fmaf_rn(v.y, v.y, cs);
                         cs = __fmaf_rn(v.z, v.z, cs); cs = __fmaf_rn(v.w, v.w, cs);
                     }
+#endif
                 ss += (double)cs;
                 if (kb + 1 == nk && r < g_valid) gate_na[g_tok0 + r] = ss;
             }
